@@ -1,0 +1,157 @@
+/*
+ * dmas.h — C ABI of the B200-native DMAS / CF beamforming hot path.
+ *
+ * Implements the beamforming stage of Jansen, Daems, Steckel, "Delay-Multiply-And-Sum
+ * Beamforming for Real-Time In-Air Acoustic Imaging" (arXiv 2511.09165).  Citations are
+ * PAPER.md:<line> of the paper's LaTeX source.  Problem statement: an array of
+ * N microphones with signals m_i(t); a set of M directions psi; a delay look-up table
+ * tau_{i,psi}; pre-steering x_i(t,psi) = m_i(t + tau_{i,psi}) (Eq. (1)); per
+ * pixel (t, psi): DAS (Eq. (2)), DMAS of order p (Eqs. (5)/(6), PAPER.md:106/116,
+ * evaluated through power sums and the Newton-Girard expansions PAPER.md:129-165), the
+ * Coherence Factor and CF-weighted image, then envelope detection
+ * (|.| then low-pass, PAPER.md:75, 5 kHz PAPER.md:253).
+ *
+ * Notation: this header writes n_mics for the paper's N and n_dirs for the paper's M.
+ *
+ * Conventions common to every call:
+ *  - No C++ types, exceptions or torch types cross this boundary.  Sizes are explicit.
+ *  - Every call returns a dmas_status; DMAS_OK = 0.  On error nothing the caller owns is
+ *    modified except as stated, and dmas_last_error() returns a one-line message
+ *    (thread-local, valid until the next call on the same thread).
+ *  - Validation errors are returned synchronously, before any device work is enqueued.
+ *    Asynchronous device faults surface as DMAS_ERR_CUDA at a later call or stream sync.
+ *  - Device pointers must belong to the plan's device and be 4-byte aligned.
+ *  - A plan is immutable after dmas_plan() (except its internal scratch); it may be used
+ *    by one in-flight dmas_beamform* call at a time (calls on one plan are serialised by
+ *    an internal mutex).  Distinct plans are independent.
+ */
+#ifndef DMAS_H
+#define DMAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dmas_plan_s* dmas_plan_t;
+
+typedef enum {
+  DMAS_OK = 0,
+  DMAS_ERR_NULL = 1,    /* a required pointer argument is NULL                                   */
+  DMAS_ERR_INVALID = 2, /* bad descriptor value: fs<=0, c<=0, n_mics<1, n_dirs<1, n_samples<1,
+                           non-finite geometry, theta not in [-pi,pi], phi not in [-pi/2,pi/2],
+                           duplicate microphone positions, lp_taps even or <0, lp_cutoff not in
+                           (0, fs/2), bp_taps even or <0, env_decim<1, cf_eps<0, delay range
+                           too large for int32 windows                                            */
+  DMAS_ERR_ORDER = 3,   /* order p not in [2,5], or n_mics < p (the DMAS sum is empty)             */
+  DMAS_ERR_SHAPE = 4,   /* n_frames<0 or > max_frames; output mask asks for nothing / for an
+                           envelope on a plan built with lp_taps == 0; misaligned pointer         */
+  DMAS_ERR_CUDA = 5,    /* CUDA runtime/launch error (message in dmas_last_error())               */
+  DMAS_ERR_OOM = 6      /* device or pinned host allocation failed                                 */
+} dmas_status;
+
+/* Output image kinds (bit order = order of the `outs` arrays below). */
+enum {
+  DMAS_KIND_DAS = 1,    /* S_DAS = sum_i x_i                              Eq. (2)   */
+  DMAS_KIND_DMAS = 2,   /* S_DMAS^(p) = E_p(s_1..s_N)                     Eq. (6)  */
+  DMAS_KIND_CFDMAS = 4, /* S_DMAS^(p) * CF  */
+  DMAS_KIND_CFDAS = 8,  /* S_DAS * CF  ("can also be applied to DAS")  */
+  DMAS_KIND_CF = 16,    /* CF = (sum x)^2 / (N sum x^2 + eps)  */
+  DMAS_KIND_ALL = 31
+};
+/* `what` = raw-stage kinds | (envelope-stage kinds << 8). */
+#define DMAS_RAW(kinds) ((uint32_t)(kinds))
+#define DMAS_ENV(kinds) (((uint32_t)(kinds)) << 8)
+
+typedef struct {
+  /* Geometry (host memory, caller-owned, copied by dmas_plan). */
+  int32_t n_mics;            /* N >= 1                                                          */
+  const double* mic_xyz;     /* [n_mics][3] metres; x = broadside, array usually in the y-z plane */
+  int64_t n_dirs;            /* M >= 1                                                          */
+  const double* dir_az_el;   /* [n_dirs][2] radians (azimuth theta from +x toward +y, elevation
+                                phi toward +z); row order = image row order                     */
+  const double* reference_xyz; /* [3] phase centre; NULL = origin                               */
+  double fs_hz;              /* sample rate, > 0                                                */
+  double c_mps;              /* speed of sound, > 0                                             */
+  int32_t order;             /* DMAS order p in [2,5]                                           */
+  int64_t n_samples;         /* T, samples per channel per frame, >= 1                          */
+  int32_t max_frames;        /* upper bound on n_frames per call, >= 1                          */
+  float cf_eps;              /* CF denominator guard, >= 0; default 1e-30        */
+  /* Envelope stage. */
+  int32_t lp_taps;           /* odd low-pass length; 0 = plan has no envelope stage; default 127 */
+  double lp_cutoff_hz;       /* (0, fs/2); default 5000; Blackman-windowed sinc, unit DC gain    */
+  int32_t bp_taps;           /* optional band-pass FIR length (odd); 0 = off (default)           */
+  const float* bp_coeffs;    /* [bp_taps] host, copied; applied before |.| as a centred FIR      */
+  int32_t env_decim;         /* R >= 1: envelope keeps samples t = 0, R, 2R, ... (ceil(T/R))     */
+  /* Runtime. */
+  int32_t device;            /* CUDA device ordinal; -1 = current device                        */
+  int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an
+                                envelope is requested without its raw image; 0 = 4 GiB         */
+} dmas_plan_desc;
+
+/* Fill `desc` with defaults (zero geometry; order 2; cf_eps 1e-30; lp 127 taps at 5 kHz;
+   bp off; env_decim 1; device -1; max_frames 1). */
+void dmas_plan_desc_init(dmas_plan_desc* desc);
+
+/* Build a plan: validates `desc`, computes the integer delay table d[psi][i] on the device
+   (A1: v = ((p_i - r) . u(psi)) * (-(fs/c)) in IEEE float64 with no FMA contraction in the
+   fixed order ((dx*ux + dy*uy) + dz*uz), rounded to nearest, ties to even; u(psi) from the
+   host libm), the low-pass taps, and the per-tile staging metadata, and allocates the
+   plan-owned signed-root scratch.  On success *out is a new plan; on error *out = NULL. */
+dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out);
+
+/* Beamform n_frames frames, asynchronously on `cuda_stream` (a cudaStream_t; NULL = legacy
+   default stream).  Returns after enqueueing.
+     signals : DEVICE, fp32 [n_frames][n_mics][n_samples], t contiguous, caller-owned, read-only.
+     outs    : HOST array of DEVICE pointers, one per requested (stage, kind): first the raw kinds
+               of `what` in bit order, then the envelope kinds in bit order.  Raw outputs are fp32
+               [n_frames][n_dirs][n_samples]; envelope outputs are fp32
+               [n_frames][n_dirs][ceil(n_samples / env_decim)].  Caller-owned, write-only.
+     what    : DMAS_RAW(kinds) | DMAS_ENV(kinds); must request at least one output.
+   Reads of m_i outside [0, n_samples) are 0.  n_frames == 0 is a no-op. */
+dmas_status dmas_beamform(dmas_plan_t plan, const float* signals, int32_t n_frames,
+                          float* const* outs, uint32_t what, void* cuda_stream);
+
+/* Same computation with HOST buffers: copies the signals in, computes, copies the images out,
+   pipelined in frame chunks over copy and compute streams; synchronous (returns when every
+   output is in host memory).  Host buffers may be pageable, but only page-locked buffers
+   (cudaHostAlloc / cudaHostRegister) overlap copies with compute.  Any n_frames >= 0 is
+   accepted (not bounded by max_frames). */
+dmas_status dmas_beamform_host(dmas_plan_t plan, const float* host_signals, int32_t n_frames,
+                               float* const* host_outs, uint32_t what);
+
+/* Copy the plan's integer delay table into host memory int32 [n_dirs][n_mics]. */
+dmas_status dmas_delay_table(dmas_plan_t plan, int32_t* host_out);
+
+typedef struct {
+  int64_t n_dirs, n_samples, n_out_samples; /* n_out_samples = ceil(T / env_decim)            */
+  int32_t n_mics, order, lp_taps, env_decim, device;
+  int32_t d_min, d_max;       /* range of the delay table (samples)                          */
+  int32_t psi_tile, t_tile;   /* beamform CTA tile: directions x samples                     */
+  int32_t window;             /* staged samples per microphone per CTA (t_tile + tile spread) */
+  int32_t chunk_frames;       /* frames per internal chunk                                   */
+} dmas_plan_info;
+dmas_status dmas_get_plan_info(dmas_plan_t plan, dmas_plan_info* info);
+
+/* Per-kernel device timing: when enabled, the plan records a CUDA event pair around every
+   kernel it launches (on the launching stream).  dmas_timing_read synchronises those events,
+   writes the summed milliseconds and launch counts per kernel (index 0 delay_table,
+   1 prologue (signed roots), 2 beamform, 3 envelope) and clears the record. */
+dmas_status dmas_set_timing(dmas_plan_t plan, int32_t enable);
+dmas_status dmas_timing_read(dmas_plan_t plan, double ms_out[4], int64_t count_out[4]);
+
+/* Total number of kernels this library has launched in the process (all plans). */
+int64_t dmas_launch_count(void);
+
+/* Destroy a plan (NULL-safe).  Synchronises the plan's device work first. */
+void dmas_destroy(dmas_plan_t plan);
+
+const char* dmas_status_string(dmas_status status);
+const char* dmas_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DMAS_H */

@@ -1,0 +1,396 @@
+// sm_100a kernels of the DMAS / CF beamforming hot path (arXiv 2511.09165).
+//
+// K1 k_delay_table  — A1 delay LUT, IEEE fp64, bit-exact with the oracle.
+// K2 k_signed_roots — A3 hoisted signed roots S = sgn(m)|m|^(1/p), once per
+//                     input sample instead of once per (mic, pixel): with integer delays
+//                     s_i(t, psi) = S_i[t + d(psi, i)] exactly.
+// K3 k_beamform     — A2 gather (Eq. (1)) + A3 power sums + A4
+//                     Newton-Girard and CF, fused.
+// K4 k_envelope_*   — A5 |.| + low-pass, optional band-pass, clamp, decimate.
+//
+// Design notes: the path is a gather-plus-reduction, so no tensor cores.
+// K3 is bound by the FP32 pipe (5 FP32 ops per mic-pixel at p = 2) with shared-memory bandwidth
+// close behind; its staging is one cp.async.bulk (TMA bulk engine) per microphone row into a
+// window reused by BF_PSI directions; packed FADD2/FFMA2 halve the issue slots of the accumulate.
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dmas_kernels.cuh"
+
+namespace dmas {
+
+// ------------------------------------------------------------------------------------------
+// K1 — delay table.  One thread per (psi, i).  Fixed op order, no FMA contraction:
+//   dot = ((px - rx)*ux + (py - ry)*uy) + (pz - rz)*uz ;  v = dot * k ;  d = rint_even(v)
+// ------------------------------------------------------------------------------------------
+__global__ void k_delay_table(const double* __restrict__ u, const double* __restrict__ pos, double rx, double ry,
+                              double rz, double k, int64_t n_dirs, int32_t n_mics, int32_t* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_dirs * (int64_t)n_mics) return;
+  const int64_t a = idx / n_mics;
+  const int32_t i = (int32_t)(idx - a * n_mics);
+  const double ux = u[3 * a], uy = u[3 * a + 1], uz = u[3 * a + 2];
+  const double dx = __dsub_rn(pos[3 * i], rx), dy = __dsub_rn(pos[3 * i + 1], ry), dz = __dsub_rn(pos[3 * i + 2], rz);
+  const double dot = __dadd_rn(__dadd_rn(__dmul_rn(dx, ux), __dmul_rn(dy, uy)), __dmul_rn(dz, uz));
+  const double v = __dmul_rn(dot, k);
+  out[idx] = __double2int_rn(v);
+}
+
+cudaError_t launch_delay_table(const double* u, const double* pos, double rx, double ry, double rz, double k,
+                               int64_t n_dirs, int32_t n_mics, int32_t* out, cudaStream_t st) {
+  const int64_t n = n_dirs * (int64_t)n_mics;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  k_delay_table<<<(unsigned)blocks, threads, 0, st>>>(u, pos, rx, ry, rz, k, n_dirs, n_mics, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 — signed-root plane.  IEEE sqrt / cbrt / pow (no fast-math): roots are taken once per
+// input sample, so their cost is amortised over every direction.
+// ------------------------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ float signed_root(float v) {
+  const float a = fabsf(v);
+  float r;
+  if (P == 2) r = __fsqrt_rn(a);
+  else if (P == 3) r = cbrtf(a);
+  else if (P == 4) r = __fsqrt_rn(__fsqrt_rn(a));
+  else r = powf(a, 0.2f);
+  return copysignf(r, v);
+}
+
+template <int P>
+__global__ void k_signed_roots(const float* __restrict__ m, float* __restrict__ S, int64_t T, int64_t Tp, int64_t G) {
+  const int64_t row = blockIdx.x;
+  const float* mr = m + row * T;
+  float* sr = S + row * Tp + G;
+  for (int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.y * blockDim.x)
+    sr[t] = signed_root<P>(__ldg(mr + t));
+}
+
+cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G,
+                                cudaStream_t st) {
+  const int threads = 256;
+  int64_t bx = (T + threads - 1) / threads;
+  if (bx > 64) bx = 64;
+  dim3 grid((unsigned)rows, (unsigned)bx);
+  switch (order) {
+    case 2: k_signed_roots<2><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 3: k_signed_roots<3><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 4: k_signed_roots<4><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 5: k_signed_roots<5><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 — fused gather + power sums + Newton-Girard + CF.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// TMA bulk copy global -> shared (1D, 16 B granules), completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Per-pixel accumulators.  P1..P_{p-1} of the signed roots, P_p (= A for odd p, = sum |x| for
+// even p), A = sum x (DAS) and B = sum x^2 (CF).  Packed in float2 pairs for FADD2/FFMA2.
+template <int P> struct Acc;
+template <> struct Acc<2> { float2 pa, pb; };          // pa = (P1, A), pb = (P2, B)
+template <> struct Acc<3> { float2 p12; float a, b; };  // P3 = A
+template <> struct Acc<4> { float2 p12, p34; float a, b; };
+template <> struct Acc<5> { float2 p12, p34; float a, b; };  // P5 = A
+
+template <int P> __device__ __forceinline__ void acc_zero(Acc<P>& c);
+template <> __device__ __forceinline__ void acc_zero<2>(Acc<2>& c) { c.pa = c.pb = make_float2(0.f, 0.f); }
+template <> __device__ __forceinline__ void acc_zero<3>(Acc<3>& c) { c.p12 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
+template <> __device__ __forceinline__ void acc_zero<4>(Acc<4>& c) { c.p12 = c.p34 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
+template <> __device__ __forceinline__ void acc_zero<5>(Acc<5>& c) { c.p12 = c.p34 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
+
+// One microphone sample s = s_i(t, psi) of one pixel.  x = sgn(s)|s|^p is rebuilt from s
+// (exact up to rounding since s^p = sgn(x)^p |x| and the p = 2 / 4 cases take |s|).
+template <int P> __device__ __forceinline__ void acc_add(Acc<P>& c, float s);
+template <> __device__ __forceinline__ void acc_add<2>(Acc<2>& c, float s) {
+  const float2 sx = make_float2(s, s * fabsf(s));   // (s, x)
+  c.pa = __fadd2_rn(c.pa, sx);                      // P1 += s, A += x
+  c.pb = __ffma2_rn(sx, sx, c.pb);                  // P2 += s^2 (= |x|), B += x^2
+}
+template <> __device__ __forceinline__ void acc_add<3>(Acc<3>& c, float s) {
+  const float s2 = s * s;
+  const float x = s2 * s;
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
+  c.a += x;
+  c.b = fmaf(x, x, c.b);
+}
+template <> __device__ __forceinline__ void acc_add<4>(Acc<4>& c, float s) {
+  const float s2 = s * s;
+  const float s3 = s2 * s;
+  const float s4 = s2 * s2;                          // = |x|
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
+  c.p34 = __fadd2_rn(c.p34, make_float2(s3, s4));
+  c.a += copysignf(s4, s);                           // x
+  c.b = fmaf(s4, s4, c.b);
+}
+template <> __device__ __forceinline__ void acc_add<5>(Acc<5>& c, float s) {
+  const float s2 = s * s;
+  const float s3 = s2 * s;
+  const float s4 = s2 * s2;
+  const float x = s4 * s;
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
+  c.p34 = __fadd2_rn(c.p34, make_float2(s3, s4));
+  c.a += x;
+  c.b = fmaf(x, x, c.b);
+}
+
+// Newton-Girard explicit expansions, exactly as printed.
+template <int P> __device__ __forceinline__ void acc_final(const Acc<P>& c, float& A, float& B, float& E);
+template <> __device__ __forceinline__ void acc_final<2>(const Acc<2>& c, float& A, float& B, float& E) {
+  const float P1 = c.pa.x, P2 = c.pb.x;
+  A = c.pa.y; B = c.pb.y;
+  E = 0.5f * (P1 * P1 - P2);
+}
+template <> __device__ __forceinline__ void acc_final<3>(const Acc<3>& c, float& A, float& B, float& E) {
+  const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.a;
+  A = c.a; B = c.b;
+  E = (P1 * P1 * P1 + 2.f * P3 - 3.f * P1 * P2) * (1.f / 6.f);
+}
+template <> __device__ __forceinline__ void acc_final<4>(const Acc<4>& c, float& A, float& B, float& E) {
+  const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.p34.x, P4 = c.p34.y;
+  A = c.a; B = c.b;
+  const float P1s = P1 * P1;
+  E = (P1s * P1s - 6.f * P4 + 3.f * P2 * P2 - 6.f * P2 * P1s + 8.f * P3 * P1) * (1.f / 24.f);
+}
+template <> __device__ __forceinline__ void acc_final<5>(const Acc<5>& c, float& A, float& B, float& E) {
+  const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.p34.x, P4 = c.p34.y, P5 = c.a;
+  A = c.a; B = c.b;
+  const float P1s = P1 * P1;
+  E = (P1s * P1s * P1 - 10.f * P2 * P1s * P1 + 15.f * P2 * P2 * P1 + 20.f * P3 * P1s - 20.f * P3 * P2 -
+       30.f * P1 * P4 + 24.f * P5) * (1.f / 120.f);
+}
+
+template <int P>
+__global__ void __launch_bounds__(BF_THREADS, 2) k_beamform(const BeamformArgs a) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const int32_t n_mics = a.n_mics, W = a.W;
+  float* win = smem;                                   // [n_mics][W]   staged S window
+  int32_t* offs = reinterpret_cast<int32_t*>(smem + (size_t)n_mics * W);  // [BF_PSI][n_mics]
+
+  const int64_t t0 = (int64_t)blockIdx.x * BF_T;
+  const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
+  const int64_t f = blockIdx.z;
+  const int npsi = (int)min((int64_t)BF_PSI, a.n_dirs - psi0);
+  const int32_t lo = __ldg(a.tile_lo + blockIdx.y);   // window origin relative to t0 (<= min delay of tile)
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t row_bytes = (uint32_t)W * 4u;
+    mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics);
+    const float* src = a.splane + (f * n_mics) * a.Tp + a.G + t0 + lo;
+    for (int i = 0; i < n_mics; ++i) bulk_g2s(win + (size_t)i * W, src + (int64_t)i * a.Tp, row_bytes, &bar);
+  }
+  // delay rows of this psi tile -> smem word offsets into the window (overlaps the TMA)
+  for (int idx = threadIdx.x; idx < npsi * n_mics; idx += BF_THREADS) {
+    const int q = idx / n_mics, i = idx - q * n_mics;
+    offs[idx] = i * W + (__ldg(a.delays + (psi0 + q) * n_mics + i) - lo);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* wl = win + lane;
+  for (int q = warp; q < npsi; q += BF_WARPS) {
+    Acc<P> acc[BF_KT];
+#pragma unroll
+    for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
+    const int32_t* oq = offs + q * n_mics;
+#pragma unroll 2
+    for (int i = 0; i < n_mics; ++i) {
+      const float* w = wl + oq[i];
+#pragma unroll
+      for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
+    }
+    const int64_t psi = psi0 + q;
+    const int64_t rowoff = (f * a.n_dirs + psi) * a.T;
+#pragma unroll
+    for (int k = 0; k < BF_KT; ++k) {
+      const int64_t t = t0 + lane + 32 * k;
+      if (t >= a.T) continue;
+      float A, B, E;
+      acc_final<P>(acc[k], A, B, E);
+      const float cf = __fdividef(A * A, fmaf(a.n_mics_f, B, a.cf_eps));
+      const int64_t o = rowoff + t;
+      if (a.out[0]) a.out[0][o] = A;
+      if (a.out[1]) a.out[1][o] = E;
+      if (a.out[2]) a.out[2][o] = E * cf;
+      if (a.out[3]) a.out[3][o] = A * cf;
+      if (a.out[4]) a.out[4][o] = cf;
+    }
+  }
+}
+
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W) {
+  return (size_t)n_mics * W * sizeof(float) + (size_t)BF_PSI * n_mics * sizeof(int32_t);
+}
+
+cudaError_t beamform_configure(int32_t n_mics, int32_t W) {
+  const int bytes = (int)beamform_smem_bytes(n_mics, W);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_beamform<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
+  const int64_t ntt = (a.T + BF_T - 1) / BF_T;
+  const int64_t npt = (a.n_dirs + BF_PSI - 1) / BF_PSI;
+  dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
+  const size_t smem = beamform_smem_bytes(a.n_mics, a.W);
+  switch (order) {
+    case 2: k_beamform<2><<<grid, BF_THREADS, smem, st>>>(a); break;
+    case 3: k_beamform<3><<<grid, BF_THREADS, smem, st>>>(a); break;
+    case 4: k_beamform<4><<<grid, BF_THREADS, smem, st>>>(a); break;
+    case 5: k_beamform<5><<<grid, BF_THREADS, smem, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// K4 fast path — 127-tap low-pass of |y|, R = 1, no band-pass.  Each thread produces 4
+// consecutive outputs from 33 float4 smem reads (130 distinct inputs); the taps live in the
+// kernel-parameter constant bank, so every MAC is one FFMA R, R, c[], R.
+//   e[t] = max(0, sum_k h[k] |y[t + 63 - k]|), zeros outside [0, T)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(ENV_THREADS) k_envelope_lp127(const float* __restrict__ y, float* __restrict__ out,
+                                                               int64_t T, const __grid_constant__ LpTaps127 taps) {
+  __shared__ __align__(16) float sa[ENV_T + 128];
+  const int64_t row = blockIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.y * ENV_T;
+  const float* yr = y + row * T;
+  for (int u = threadIdx.x; u < ENV_T + 128; u += ENV_THREADS) {
+    const int64_t t = t0 - 64 + u;                     // sa[u] = |y[t0 - 64 + u]|
+    sa[u] = (t >= 0 && t < T) ? fabsf(__ldg(yr + t)) : 0.f;
+  }
+  __syncthreads();
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const float4* a4 = reinterpret_cast<const float4*>(sa) + threadIdx.x;
+#pragma unroll
+  for (int v = 0; v < 33; ++v) {
+    const float4 q = a4[v];
+    const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int u = 4 * v + c;                         // sample t0 + 4 tid - 64 + u
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = j + 127 - u;                     // output t0 + 4 tid + j uses tap k
+        if (k >= 0 && k < ENV_FAST_TAPS) acc[j] = fmaf(taps.h[k], e[c], acc[j]);
+      }
+    }
+  }
+  const int64_t tb = t0 + 4 * threadIdx.x;
+  float* orow = out + row * T;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (tb + j < T) orow[tb + j] = fmaxf(acc[j], 0.f);
+}
+
+cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
+                                  cudaStream_t st) {
+  dim3 grid((unsigned)rows, (unsigned)((T + ENV_T - 1) / ENV_T));
+  k_envelope_lp127<<<grid, ENV_THREADS, 0, st>>>(y, out, T, taps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// K4 generic path — any odd L, optional band-pass (odd Lb), decimation R.
+//   b[s] = |sum_k bp[k] y[s + cb - k]| (or |y[s]|) for s in [0, T), 0 outside
+//   out[o] = max(0, sum_k lp[k] b[R o + c - k])
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(ENV_THREADS) k_envelope_generic(const float* __restrict__ y, float* __restrict__ out,
+                                                                 int64_t T, int64_t T_out, int32_t R,
+                                                                 const float* __restrict__ lp, int32_t L,
+                                                                 const float* __restrict__ bp, int32_t Lb) {
+  extern __shared__ __align__(16) float sh[];
+  const int c = (L - 1) / 2, cb = Lb > 0 ? (Lb - 1) / 2 : 0;
+  const int64_t row = blockIdx.x;
+  const int64_t o0 = (int64_t)blockIdx.y * ENV_GEN_T;
+  const int64_t o_end = min(o0 + ENV_GEN_T, T_out);
+  const int64_t s_lo = o0 * R - c;
+  const int nb = (int)((o_end - 1) * R + c - s_lo + 1);
+  float* b = sh;
+  const float* yr = y + row * T;
+  if (Lb > 0) {
+    float* yy = sh + nb;                                 // y over [s_lo - cb, s_lo + nb + cb)
+    for (int u = threadIdx.x; u < nb + 2 * cb; u += blockDim.x) {
+      const int64_t s = s_lo - cb + u;
+      yy[u] = (s >= 0 && s < T) ? __ldg(yr + s) : 0.f;
+    }
+    __syncthreads();
+    for (int u = threadIdx.x; u < nb; u += blockDim.x) {
+      const int64_t s = s_lo + u;
+      float acc = 0.f;
+      if (s >= 0 && s < T)
+        for (int k = 0; k < Lb; ++k) acc = fmaf(__ldg(bp + k), yy[u + 2 * cb - k], acc);
+      b[u] = fabsf(acc);
+    }
+  } else {
+    for (int u = threadIdx.x; u < nb; u += blockDim.x) {
+      const int64_t s = s_lo + u;
+      b[u] = (s >= 0 && s < T) ? fabsf(__ldg(yr + s)) : 0.f;
+    }
+  }
+  __syncthreads();
+  for (int64_t o = o0 + threadIdx.x; o < o_end; o += blockDim.x) {
+    const int base = (int)(o * R - s_lo) + c;            // index of sample R o + c in b
+    float acc = 0.f;
+    for (int k = 0; k < L; ++k) acc = fmaf(__ldg(lp + k), b[base - k], acc);
+    out[row * T_out + o] = fmaxf(acc, 0.f);
+  }
+}
+
+cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out, int32_t decim,
+                                    const float* lp, int32_t L, const float* bp, int32_t Lb, cudaStream_t st) {
+  const int c = (L - 1) / 2, cb = Lb > 0 ? (Lb - 1) / 2 : 0;
+  const int64_t nb = (int64_t)(ENV_GEN_T - 1) * decim + 2 * c + 1;
+  const size_t smem = (size_t)(nb + (Lb > 0 ? nb + 2 * cb : 0)) * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_envelope_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)rows, (unsigned)((T_out + ENV_GEN_T - 1) / ENV_GEN_T));
+  k_envelope_generic<<<grid, ENV_THREADS, smem, st>>>(y, out, T, T_out, decim, lp, L, bp, Lb);
+  return cudaGetLastError();
+}
+
+}  // namespace dmas

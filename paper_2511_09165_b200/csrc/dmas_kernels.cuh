@@ -1,0 +1,58 @@
+// Internal launcher interface between the plan runtime (dmas_plan.cpp) and the sm_100a kernels
+// (dmas_kernels.cu).  Not part of the public ABI (include/dmas.h is).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dmas {
+
+// Beamform CTA tile (K3): BF_PSI directions x BF_T samples; 8 warps, lanes over t, 8 t / lane.
+constexpr int BF_THREADS = 256;
+constexpr int BF_WARPS = BF_THREADS / 32;
+constexpr int BF_T = 256;
+constexpr int BF_KT = BF_T / 32;
+constexpr int BF_PSI = 32;
+
+// Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
+constexpr int ENV_THREADS = 256;
+constexpr int ENV_T = 1024;
+constexpr int ENV_FAST_TAPS = 127;
+constexpr int ENV_GEN_T = 256;          // generic path: outputs per CTA
+
+constexpr int N_KINDS = 5;              // DAS, DMAS, CFDMAS, CFDAS, CF (dmas.h bit order)
+
+struct BeamformArgs {
+  const float* splane;      // [frames][n_mics][Tp]; sample t of (f, i) at column G + t; zero guards
+  const int32_t* delays;    // [n_dirs][n_mics] int32 sample delays d[psi][i]
+  const int32_t* tile_lo;   // [n_psi_tiles] window origin (relative to t0) of each psi tile, %4 == 0
+  float* out[N_KINDS];      // raw-image destinations [frames][n_dirs][T] (nullptr = kind not written)
+  int64_t Tp, G, T, n_dirs;
+  int32_t n_mics, W;        // W = staged samples per mic row (multiple of 4)
+  float n_mics_f, cf_eps;
+};
+
+struct LpTaps127 { float h[128]; };
+
+// K1: d[psi][i] = rint_even(((p_i - r) . u_psi) * k) in IEEE fp64, no contraction (A1).
+cudaError_t launch_delay_table(const double* u /*[n_dirs][3]*/, const double* pos /*[n_mics][3]*/,
+                               double rx, double ry, double rz, double k, int64_t n_dirs, int32_t n_mics,
+                               int32_t* out, cudaStream_t st);
+
+// K2: S[f][i][G + t] = sgn(m) |m|^(1/p) for t in [0, T) (hoisted signed roots, A3).
+cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp,
+                                int64_t G, cudaStream_t st);
+
+// K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
+cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W);
+cudaError_t beamform_configure(int32_t n_mics, int32_t W);   // opt-in to > 48 KB dynamic smem
+
+// K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).
+cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
+                                  cudaStream_t st);
+cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out,
+                                    int32_t decim, const float* lp, int32_t L, const float* bp, int32_t Lb,
+                                    cudaStream_t st);
+
+}  // namespace dmas

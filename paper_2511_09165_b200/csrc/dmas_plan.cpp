@@ -1,0 +1,670 @@
+// Host runtime behind include/dmas.h: plan validation and construction, per-call chunking,
+// the host-buffer copy/compute pipeline, per-kernel event timing, error reporting.
+//
+// Compiled with -ffp-contract=off: the unit vectors u(psi) (A1) must round exactly like the
+// oracle's Python `math` expression  (cos(el)*cos(az), cos(el)*sin(az), sin(el)).
+
+#include "dmas.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "dmas_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+dmas_status fail(dmas_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                             \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      return fail(e_ == cudaErrorMemoryAllocation ? DMAS_ERR_OOM : DMAS_ERR_CUDA,                  \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                             \
+    }                                                                                              \
+  } while (0)
+
+enum { K_DELAY = 0, K_ROOTS = 1, K_BEAMFORM = 2, K_ENVELOPE = 3 };
+
+struct TimingRec {
+  int kernel;
+  cudaEvent_t ev0, ev1;
+};
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int popcount5(uint32_t k) {
+  int n = 0;
+  for (int b = 0; b < dmas::N_KINDS; ++b) n += (k >> b) & 1u;
+  return n;
+}
+
+}  // namespace
+
+struct dmas_plan_s {
+  std::mutex mu;
+  int device = 0;
+  int32_t n_mics = 0, order = 2, lp_taps = 0, bp_taps = 0, env_decim = 1, max_frames = 1;
+  int64_t n_dirs = 0, T = 0, T_out = 0;
+  double fs = 0, c = 0;
+  float cf_eps = 1e-30f;
+  int32_t dmin = 0, dmax = 0;
+  std::vector<int32_t> h_delays;      // [n_dirs][n_mics]
+  std::vector<float> h_lp, h_bp;
+  dmas::LpTaps127 lp127{};
+  bool lp_fast = false;
+
+  // device state
+  int32_t* d_delays = nullptr;
+  int32_t* d_tile_lo = nullptr;
+  int32_t W = 0;                      // staged window per mic (beamform)
+  int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
+  int32_t chunk_cap = 1;              // frames the signed-root plane holds
+  float* d_splane = nullptr;
+  float* d_lp = nullptr;
+  float* d_bp = nullptr;
+  float* d_scratch = nullptr;         // raw images of envelope-only kinds
+  size_t scratch_cap = 0;
+  int64_t scratch_budget = 0;
+
+  // host pipeline buffers (dmas_beamform_host)
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+  float* d_hsig[2] = {nullptr, nullptr};
+  float* d_hout[2] = {nullptr, nullptr};
+  size_t hsig_cap = 0, hout_cap = 0;
+
+  // timing
+  bool timing = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+
+  cudaEvent_t get_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+
+// Timed launch helper: records an event pair around `fn` when the plan's timing is on.
+template <class F>
+cudaError_t timed(dmas_plan_s* p, int kernel, cudaStream_t st, F&& fn) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing) {
+    e0 = p->get_event();
+    e1 = p->get_event();
+    cudaEventRecord(e0, st);
+  }
+  cudaError_t e = fn();
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (p->timing) {
+    cudaEventRecord(e1, st);
+    p->recs.push_back({kernel, e0, e1});
+  }
+  return e;
+}
+
+void free_plan_memory(dmas_plan_s* p) {
+  cudaFree(p->d_delays);
+  cudaFree(p->d_tile_lo);
+  cudaFree(p->d_splane);
+  cudaFree(p->d_lp);
+  cudaFree(p->d_bp);
+  cudaFree(p->d_scratch);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(p->d_hsig[b]);
+    cudaFree(p->d_hout[b]);
+  }
+  for (auto& s : p->hs)
+    if (s) cudaStreamDestroy(s);
+  for (auto& r : p->recs) {
+    cudaEventDestroy(r.ev0);
+    cudaEventDestroy(r.ev1);
+  }
+  for (auto e : p->ev_pool) cudaEventDestroy(e);
+}
+
+// Blackman-windowed sinc low-pass, unit DC gain (reading Q11):
+// h[n] = (2fc/fs) sinc((2fc/fs)(n - (L-1)/2)) w[n], w = 0.42 - 0.5cos(2 pi n/(L-1)) + 0.08cos(4 pi n/(L-1))
+std::vector<double> blackman_lowpass(int L, double fc, double fs) {
+  std::vector<double> h(L);
+  const double fcn = 2.0 * fc / fs;
+  double sum = 0.0;
+  for (int n = 0; n < L; ++n) {
+    const double x = fcn * (n - (L - 1) / 2.0);
+    const double sinc = (x == 0.0) ? 1.0 : std::sin(M_PI * x) / (M_PI * x);
+    const double w = (L > 1) ? 0.42 - 0.5 * std::cos(2.0 * M_PI * n / (L - 1)) + 0.08 * std::cos(4.0 * M_PI * n / (L - 1))
+                             : 1.0;
+    h[n] = fcn * sinc * w;
+    sum += h[n];
+  }
+  for (auto& v : h) v /= sum;
+  return h;
+}
+
+bool finite3(const double* v) { return std::isfinite(v[0]) && std::isfinite(v[1]) && std::isfinite(v[2]); }
+
+dmas_status validate(const dmas_plan_desc* d) {
+  if (!d) return fail(DMAS_ERR_NULL, "desc is NULL");
+  if (!d->mic_xyz) return fail(DMAS_ERR_NULL, "mic_xyz is NULL");
+  if (!d->dir_az_el) return fail(DMAS_ERR_NULL, "dir_az_el is NULL");
+  if (d->n_mics < 1) return fail(DMAS_ERR_INVALID, "n_mics < 1");
+  if (d->n_dirs < 1) return fail(DMAS_ERR_INVALID, "n_dirs < 1");
+  if (d->n_dirs > (int64_t)65535 * dmas::BF_PSI) return fail(DMAS_ERR_INVALID, "n_dirs too large");
+  if (d->n_samples < 1) return fail(DMAS_ERR_INVALID, "n_samples < 1");
+  if (d->n_samples > ((int64_t)1 << 30)) return fail(DMAS_ERR_INVALID, "n_samples too large");
+  if (!(d->fs_hz > 0) || !std::isfinite(d->fs_hz)) return fail(DMAS_ERR_INVALID, "fs_hz must be > 0");
+  if (!(d->c_mps > 0) || !std::isfinite(d->c_mps)) return fail(DMAS_ERR_INVALID, "c_mps must be > 0");
+  if (d->order < 2 || d->order > 5) return fail(DMAS_ERR_ORDER, "order must be in [2,5]");
+  if (d->n_mics < d->order) return fail(DMAS_ERR_ORDER, "n_mics < order (N < n)");
+  if (d->max_frames < 1 || d->max_frames > 65535) return fail(DMAS_ERR_INVALID, "max_frames not in [1,65535]");
+  if (!(d->cf_eps >= 0.0f) || !std::isfinite(d->cf_eps)) return fail(DMAS_ERR_INVALID, "cf_eps must be >= 0");
+  if (d->lp_taps < 0 || (d->lp_taps > 0 && d->lp_taps % 2 == 0) || d->lp_taps > 4095)
+    return fail(DMAS_ERR_INVALID, "lp_taps must be 0 or odd (<= 4095)");
+  if (d->lp_taps > 0 && !(d->lp_cutoff_hz > 0 && d->lp_cutoff_hz < d->fs_hz / 2))
+    return fail(DMAS_ERR_INVALID, "lp_cutoff_hz must be in (0, fs/2)");
+  if (d->bp_taps < 0 || (d->bp_taps > 0 && d->bp_taps % 2 == 0) || d->bp_taps > 4095)
+    return fail(DMAS_ERR_INVALID, "bp_taps must be 0 or odd (<= 4095)");
+  if (d->bp_taps > 0 && !d->bp_coeffs) return fail(DMAS_ERR_NULL, "bp_coeffs is NULL");
+  if (d->bp_taps > 0 && d->lp_taps == 0) return fail(DMAS_ERR_INVALID, "band-pass needs the envelope stage");
+  if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
+  if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
+  for (int i = 0; i < d->n_mics; ++i)
+    if (!finite3(d->mic_xyz + 3 * i)) return fail(DMAS_ERR_INVALID, "non-finite microphone position");
+  if (d->reference_xyz && !finite3(d->reference_xyz)) return fail(DMAS_ERR_INVALID, "non-finite reference");
+  for (int i = 0; i < d->n_mics; ++i)
+    for (int j = i + 1; j < d->n_mics; ++j) {
+      const double* a = d->mic_xyz + 3 * i;
+      const double* b = d->mic_xyz + 3 * j;
+      if (a[0] == b[0] && a[1] == b[1] && a[2] == b[2]) return fail(DMAS_ERR_INVALID, "duplicate microphone positions");
+    }
+  const double tol = 1e-12;
+  for (int64_t a = 0; a < d->n_dirs; ++a) {
+    const double az = d->dir_az_el[2 * a], el = d->dir_az_el[2 * a + 1];
+    if (!std::isfinite(az) || !std::isfinite(el)) return fail(DMAS_ERR_INVALID, "non-finite direction");
+    if (az < -M_PI - tol || az > M_PI + tol) return fail(DMAS_ERR_INVALID, "azimuth not in [-pi, pi]");
+    if (el < -M_PI / 2 - tol || el > M_PI / 2 + tol) return fail(DMAS_ERR_INVALID, "elevation not in [-pi/2, pi/2]");
+  }
+  return DMAS_OK;
+}
+
+// Enqueue one chunk of frames: roots -> beamform -> envelopes.  `sig` / `outs_raw` / `outs_env`
+// already point at the chunk's first frame.
+dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* const* raw_dst,
+                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st) {
+  CUDA_TRY(timed(p, K_ROOTS, st, [&] {
+    return dmas::launch_signed_roots(p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
+  }));
+  dmas::BeamformArgs a{};
+  a.splane = p->d_splane;
+  a.delays = p->d_delays;
+  a.tile_lo = p->d_tile_lo;
+  for (int k = 0; k < dmas::N_KINDS; ++k) a.out[k] = raw_dst[k];
+  a.Tp = p->Tp;
+  a.G = p->G;
+  a.T = p->T;
+  a.n_dirs = p->n_dirs;
+  a.n_mics = p->n_mics;
+  a.W = p->W;
+  a.n_mics_f = (float)p->n_mics;
+  a.cf_eps = p->cf_eps;
+  CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
+  const int64_t rows = (int64_t)nf * p->n_dirs;
+  for (int k = 0; k < dmas::N_KINDS; ++k) {
+    if (!((env_kinds >> k) & 1u)) continue;
+    const float* y = raw_dst[k];
+    float* o = env_dst[k];
+    if (p->lp_fast) {
+      CUDA_TRY(timed(p, K_ENVELOPE, st, [&] { return dmas::launch_envelope_lp127(y, o, rows, p->T, p->lp127, st); }));
+    } else {
+      CUDA_TRY(timed(p, K_ENVELOPE, st, [&] {
+        return dmas::launch_envelope_generic(y, o, rows, p->T, p->T_out, p->env_decim, p->d_lp, p->lp_taps, p->d_bp,
+                                             p->bp_taps, st);
+      }));
+    }
+  }
+  return DMAS_OK;
+}
+
+dmas_status check_what(dmas_plan_s* p, uint32_t what, uint32_t& raw_k, uint32_t& env_k) {
+  raw_k = what & DMAS_KIND_ALL;
+  env_k = (what >> 8) & DMAS_KIND_ALL;
+  if (what & ~(uint32_t)(DMAS_RAW(DMAS_KIND_ALL) | DMAS_ENV(DMAS_KIND_ALL)))
+    return fail(DMAS_ERR_SHAPE, "unknown bits in `what`");
+  if (!raw_k && !env_k) return fail(DMAS_ERR_SHAPE, "`what` requests no output");
+  if (env_k && p->lp_taps == 0) return fail(DMAS_ERR_SHAPE, "envelope requested on a plan without envelope stage");
+  return DMAS_OK;
+}
+
+// Core of dmas_beamform on device pointers (caller holds p->mu and the device guard).
+dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_frames, float* const* outs,
+                            uint32_t raw_k, uint32_t env_k, cudaStream_t st) {
+  const float* raw_user[dmas::N_KINDS] = {};
+  float* env_user[dmas::N_KINDS] = {};
+  int n = 0;
+  for (int k = 0; k < dmas::N_KINDS; ++k)
+    if ((raw_k >> k) & 1u) raw_user[k] = outs[n++];
+  for (int k = 0; k < dmas::N_KINDS; ++k)
+    if ((env_k >> k) & 1u) env_user[k] = outs[n++];
+  for (int i = 0; i < n; ++i) {
+    if (!outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
+    if (((uintptr_t)outs[i]) & 3u) return fail(DMAS_ERR_SHAPE, "misaligned output pointer");
+  }
+  // envelope kinds without their raw image go through the plan's scratch
+  const uint32_t env_only = env_k & ~raw_k;
+  const int n_scratch = popcount5(env_only);
+  const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
+  int32_t chunk = std::min(p->chunk_cap, n_frames);
+  if (n_scratch > 0) {
+    const int64_t fit = p->scratch_budget / (int64_t)(frame_img * n_scratch);
+    chunk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(chunk, fit));
+    const size_t need = (size_t)chunk * n_scratch * frame_img;
+    if (need > p->scratch_cap) {
+      CUDA_TRY(cudaStreamSynchronize(st));
+      cudaFree(p->d_scratch);
+      p->d_scratch = nullptr;
+      p->scratch_cap = 0;
+      CUDA_TRY(cudaMalloc(&p->d_scratch, need));
+      p->scratch_cap = need;
+    }
+  }
+  for (int32_t f0 = 0; f0 < n_frames; f0 += chunk) {
+    const int32_t nf = std::min(chunk, n_frames - f0);
+    float* raw_dst[dmas::N_KINDS] = {};
+    float* env_dst[dmas::N_KINDS] = {};
+    int s = 0;
+    for (int k = 0; k < dmas::N_KINDS; ++k) {
+      if ((raw_k >> k) & 1u) raw_dst[k] = const_cast<float*>(raw_user[k]) + (size_t)f0 * p->n_dirs * p->T;
+      else if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
+      if ((env_k >> k) & 1u) env_dst[k] = env_user[k] + (size_t)f0 * p->n_dirs * p->T_out;
+    }
+    const float* sig = signals + (size_t)f0 * p->n_mics * p->T;
+    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st);
+    if (rc != DMAS_OK) return rc;
+  }
+  return DMAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void dmas_plan_desc_init(dmas_plan_desc* d) {
+  if (!d) return;
+  std::memset(d, 0, sizeof(*d));
+  d->order = 2;
+  d->max_frames = 1;
+  d->cf_eps = 1e-30f;
+  d->lp_taps = 127;
+  d->lp_cutoff_hz = 5000.0;
+  d->env_decim = 1;
+  d->device = -1;
+}
+
+dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
+  if (!out) return fail(DMAS_ERR_NULL, "out is NULL");
+  *out = nullptr;
+  dmas_status st = validate(desc);
+  if (st != DMAS_OK) return st;
+
+  int dev = desc->device;
+  if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (dev >= ndev) return fail(DMAS_ERR_INVALID, "device ordinal out of range");
+  DeviceGuard guard(dev);
+
+  auto* p = new dmas_plan_s();
+  p->device = dev;
+  p->n_mics = desc->n_mics;
+  p->n_dirs = desc->n_dirs;
+  p->T = desc->n_samples;
+  p->order = desc->order;
+  p->max_frames = desc->max_frames;
+  p->fs = desc->fs_hz;
+  p->c = desc->c_mps;
+  p->cf_eps = desc->cf_eps;
+  p->lp_taps = desc->lp_taps;
+  p->bp_taps = desc->bp_taps;
+  p->env_decim = desc->env_decim;
+  p->T_out = (p->T + p->env_decim - 1) / p->env_decim;
+  p->scratch_budget = desc->scratch_bytes > 0 ? desc->scratch_bytes : ((int64_t)4 << 30);
+
+  auto bail = [&](dmas_status s) {
+    free_plan_memory(p);
+    delete p;
+    return s;
+  };
+#define PLAN_TRY(expr)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? DMAS_ERR_OOM : DMAS_ERR_CUDA,            \
+                       std::string(#expr) + ": " + cudaGetErrorString(e_)));                      \
+  } while (0)
+
+  // ---- A1: unit vectors on the host (libm, no contraction), table on the device
+  const int64_t nd = p->n_dirs;
+  const int32_t nm = p->n_mics;
+  std::vector<double> u((size_t)nd * 3);
+  for (int64_t a = 0; a < nd; ++a) {
+    const double az = desc->dir_az_el[2 * a], el = desc->dir_az_el[2 * a + 1];
+    const double ce = std::cos(el);
+    u[3 * a] = ce * std::cos(az);
+    u[3 * a + 1] = ce * std::sin(az);
+    u[3 * a + 2] = std::sin(el);
+  }
+  const double rx = desc->reference_xyz ? desc->reference_xyz[0] : 0.0;
+  const double ry = desc->reference_xyz ? desc->reference_xyz[1] : 0.0;
+  const double rz = desc->reference_xyz ? desc->reference_xyz[2] : 0.0;
+  // |v| <= |p - r| fs / c must fit comfortably in int32 windows
+  double rmax = 0.0;
+  for (int i = 0; i < nm; ++i) {
+    const double* q = desc->mic_xyz + 3 * i;
+    rmax = std::max(rmax, std::sqrt((q[0] - rx) * (q[0] - rx) + (q[1] - ry) * (q[1] - ry) + (q[2] - rz) * (q[2] - rz)));
+  }
+  if (rmax * p->fs / p->c > 1.0e6) return bail(fail(DMAS_ERR_INVALID, "delay range exceeds 1e6 samples"));
+  const double k = -(p->fs / p->c);
+
+  double* d_u = nullptr;
+  double* d_pos = nullptr;
+  PLAN_TRY(cudaMalloc(&d_u, u.size() * sizeof(double)));
+  PLAN_TRY(cudaMalloc(&d_pos, (size_t)nm * 3 * sizeof(double)));
+  PLAN_TRY(cudaMalloc(&p->d_delays, (size_t)nd * nm * sizeof(int32_t)));
+  PLAN_TRY(cudaMemcpy(d_u, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice));
+  PLAN_TRY(cudaMemcpy(d_pos, desc->mic_xyz, (size_t)nm * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  PLAN_TRY(timed(p, K_DELAY, nullptr,
+                 [&] { return dmas::launch_delay_table(d_u, d_pos, rx, ry, rz, k, nd, nm, p->d_delays, nullptr); }));
+  p->h_delays.resize((size_t)nd * nm);
+  PLAN_TRY(cudaMemcpy(p->h_delays.data(), p->d_delays, p->h_delays.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  cudaFree(d_u);
+  cudaFree(d_pos);
+
+  // ---- beamform staging metadata: per psi tile window origin (aligned down to 4) and width
+  const int64_t n_pt = (nd + dmas::BF_PSI - 1) / dmas::BF_PSI;
+  std::vector<int32_t> tile_lo((size_t)n_pt);
+  p->dmin = INT32_MAX;
+  p->dmax = INT32_MIN;
+  int32_t wmax = 0, lo_min = INT32_MAX, lo_max = INT32_MIN;
+  for (int64_t t = 0; t < n_pt; ++t) {
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BF_PSI);
+    for (int64_t a = t * dmas::BF_PSI; a < a1; ++a)
+      for (int i = 0; i < nm; ++i) {
+        const int32_t v = p->h_delays[(size_t)a * nm + i];
+        lo = std::min(lo, v);
+        hi = std::max(hi, v);
+      }
+    p->dmin = std::min(p->dmin, lo);
+    p->dmax = std::max(p->dmax, hi);
+    const int32_t lo_al = (int32_t)(std::floor(lo / 4.0) * 4);
+    tile_lo[(size_t)t] = lo_al;
+    lo_min = std::min(lo_min, lo_al);
+    lo_max = std::max(lo_max, lo_al);
+    wmax = std::max(wmax, dmas::BF_T + (hi - lo_al));
+  }
+  p->W = (wmax + 3) / 4 * 4;
+  const size_t smem = dmas::beamform_smem_bytes(nm, p->W);
+  int smem_optin = 0;
+  PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem + 64 > (size_t)smem_optin)
+    return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
+                                           std::to_string(smem) + " B)"));
+  PLAN_TRY(dmas::beamform_configure(nm, p->W));
+  PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
+  PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+
+  // ---- signed-root plane with zero guards: reads at t + d outside [0, T) return 0 (reading Q5)
+  p->G = std::max<int64_t>(0, -(int64_t)lo_min);
+  p->G = (p->G + 3) / 4 * 4;
+  const int64_t ntt = (p->T + dmas::BF_T - 1) / dmas::BF_T;
+  p->Tp = p->G + (ntt - 1) * dmas::BF_T + std::max<int64_t>(0, lo_max) + p->W;
+  p->Tp = std::max<int64_t>(p->Tp, p->G + p->T);
+  p->Tp = (p->Tp + 3) / 4 * 4;
+  const size_t plane_frame = (size_t)nm * p->Tp * sizeof(float);
+  const size_t plane_budget = (size_t)256 << 20;
+  p->chunk_cap = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)p->max_frames, plane_budget / plane_frame));
+  PLAN_TRY(cudaMalloc(&p->d_splane, plane_frame * p->chunk_cap));
+  PLAN_TRY(cudaMemset(p->d_splane, 0, plane_frame * p->chunk_cap));
+
+  // ---- envelope taps
+  if (p->lp_taps > 0) {
+    std::vector<double> h = blackman_lowpass(p->lp_taps, desc->lp_cutoff_hz, p->fs);
+    p->h_lp.assign(h.begin(), h.end());
+    PLAN_TRY(cudaMalloc(&p->d_lp, p->h_lp.size() * sizeof(float)));
+    PLAN_TRY(cudaMemcpy(p->d_lp, p->h_lp.data(), p->h_lp.size() * sizeof(float), cudaMemcpyHostToDevice));
+    if (p->bp_taps > 0) {
+      p->h_bp.assign(desc->bp_coeffs, desc->bp_coeffs + p->bp_taps);
+      PLAN_TRY(cudaMalloc(&p->d_bp, p->h_bp.size() * sizeof(float)));
+      PLAN_TRY(cudaMemcpy(p->d_bp, p->h_bp.data(), p->h_bp.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    p->lp_fast = (p->lp_taps == dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1);
+    if (p->lp_fast)
+      for (int i = 0; i < dmas::ENV_FAST_TAPS; ++i) p->lp127.h[i] = p->h_lp[i];
+  }
+  PLAN_TRY(cudaDeviceSynchronize());
+#undef PLAN_TRY
+  *out = p;
+  return DMAS_OK;
+}
+
+dmas_status dmas_beamform(dmas_plan_t p, const float* signals, int32_t n_frames, float* const* outs, uint32_t what,
+                          void* cuda_stream) {
+  if (!p) return fail(DMAS_ERR_NULL, "plan is NULL");
+  if (n_frames < 0 || n_frames > p->max_frames) return fail(DMAS_ERR_SHAPE, "n_frames not in [0, max_frames]");
+  uint32_t raw_k, env_k;
+  dmas_status st = check_what(p, what, raw_k, env_k);
+  if (st != DMAS_OK) return st;
+  if (n_frames == 0) return DMAS_OK;
+  if (!signals) return fail(DMAS_ERR_NULL, "signals is NULL");
+  if (!outs) return fail(DMAS_ERR_NULL, "outs is NULL");
+  if (((uintptr_t)signals) & 3u) return fail(DMAS_ERR_SHAPE, "misaligned signals pointer");
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard guard(p->device);
+  return beamform_device(p, signals, n_frames, outs, raw_k, env_k, (cudaStream_t)cuda_stream);
+}
+
+dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t n_frames, float* const* host_outs,
+                               uint32_t what) {
+  if (!p) return fail(DMAS_ERR_NULL, "plan is NULL");
+  if (n_frames < 0) return fail(DMAS_ERR_SHAPE, "n_frames < 0");
+  uint32_t raw_k, env_k;
+  dmas_status st = check_what(p, what, raw_k, env_k);
+  if (st != DMAS_OK) return st;
+  if (n_frames == 0) return DMAS_OK;
+  if (!host_signals || !host_outs) return fail(DMAS_ERR_NULL, "host buffer is NULL");
+  const int n_out = popcount5(raw_k) + popcount5(env_k);
+  for (int i = 0; i < n_out; ++i)
+    if (!host_outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard guard(p->device);
+
+  // frames per pipeline stage: bounded by max_frames and ~512 MiB of device output per buffer
+  std::vector<size_t> out_frame_bytes;
+  size_t out_frame_total = 0;
+  for (int k = 0; k < dmas::N_KINDS; ++k)
+    if ((raw_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs * p->T * sizeof(float));
+  for (int k = 0; k < dmas::N_KINDS; ++k)
+    if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs * p->T_out * sizeof(float));
+  for (size_t b : out_frame_bytes) out_frame_total += b;
+  const size_t sig_frame = (size_t)p->n_mics * p->T * sizeof(float);
+  int32_t hc = (int32_t)std::max<size_t>(1, ((size_t)512 << 20) / out_frame_total);
+  hc = std::min({hc, p->max_frames, n_frames});
+
+  for (auto& s : p->hs)
+    if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (p->hsig_cap < sig_frame * hc || p->hout_cap < out_frame_total * hc) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(p->d_hsig[b]);
+      cudaFree(p->d_hout[b]);
+      p->d_hsig[b] = p->d_hout[b] = nullptr;
+    }
+    p->hsig_cap = p->hout_cap = 0;
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(cudaMalloc(&p->d_hsig[b], sig_frame * hc));
+      CUDA_TRY(cudaMalloc(&p->d_hout[b], out_frame_total * hc));
+    }
+    p->hsig_cap = sig_frame * hc;
+    p->hout_cap = out_frame_total * hc;
+  }
+  cudaEvent_t h2d_done[2], comp_done[2], d2h_done[2];
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(cudaEventCreateWithFlags(&h2d_done[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&comp_done[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&d2h_done[b], cudaEventDisableTiming));
+  }
+  dmas_status rc = DMAS_OK;
+  int chunk_idx = 0;
+  for (int32_t f0 = 0; f0 < n_frames && rc == DMAS_OK; f0 += hc, ++chunk_idx) {
+    const int b = chunk_idx & 1;
+    const int32_t nf = std::min(hc, n_frames - f0);
+    if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[0], d2h_done[b], 0));
+    CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T, sig_frame * nf,
+                             cudaMemcpyHostToDevice, p->hs[0]));
+    CUDA_TRY(cudaEventRecord(h2d_done[b], p->hs[0]));
+    CUDA_TRY(cudaStreamWaitEvent(p->hs[1], h2d_done[b], 0));
+    if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[1], d2h_done[b], 0));
+    std::vector<float*> douts(out_frame_bytes.size());
+    size_t off = 0;
+    for (size_t i = 0; i < out_frame_bytes.size(); ++i) {
+      douts[i] = p->d_hout[b] + off / sizeof(float);
+      off += out_frame_bytes[i] * nf;
+    }
+    rc = beamform_device(p, p->d_hsig[b], nf, douts.data(), raw_k, env_k, p->hs[1]);
+    if (rc != DMAS_OK) break;
+    CUDA_TRY(cudaEventRecord(comp_done[b], p->hs[1]));
+    CUDA_TRY(cudaStreamWaitEvent(p->hs[2], comp_done[b], 0));
+    for (size_t i = 0; i < out_frame_bytes.size(); ++i)
+      CUDA_TRY(cudaMemcpyAsync(host_outs[i] + (size_t)f0 * (out_frame_bytes[i] / sizeof(float)), douts[i],
+                               out_frame_bytes[i] * nf, cudaMemcpyDeviceToHost, p->hs[2]));
+    CUDA_TRY(cudaEventRecord(d2h_done[b], p->hs[2]));
+  }
+  cudaError_t e = cudaStreamSynchronize(p->hs[2]);
+  cudaStreamSynchronize(p->hs[1]);
+  cudaStreamSynchronize(p->hs[0]);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(h2d_done[b]);
+    cudaEventDestroy(comp_done[b]);
+    cudaEventDestroy(d2h_done[b]);
+  }
+  if (rc != DMAS_OK) return rc;
+  if (e != cudaSuccess) return fail(DMAS_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
+  return DMAS_OK;
+}
+
+dmas_status dmas_delay_table(dmas_plan_t p, int32_t* host_out) {
+  if (!p || !host_out) return fail(DMAS_ERR_NULL, "NULL argument");
+  std::memcpy(host_out, p->h_delays.data(), p->h_delays.size() * sizeof(int32_t));
+  return DMAS_OK;
+}
+
+dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
+  if (!p || !info) return fail(DMAS_ERR_NULL, "NULL argument");
+  info->n_dirs = p->n_dirs;
+  info->n_samples = p->T;
+  info->n_out_samples = p->T_out;
+  info->n_mics = p->n_mics;
+  info->order = p->order;
+  info->lp_taps = p->lp_taps;
+  info->env_decim = p->env_decim;
+  info->device = p->device;
+  info->d_min = p->dmin;
+  info->d_max = p->dmax;
+  info->psi_tile = dmas::BF_PSI;
+  info->t_tile = dmas::BF_T;
+  info->window = p->W;
+  info->chunk_frames = p->chunk_cap;
+  return DMAS_OK;
+}
+
+dmas_status dmas_set_timing(dmas_plan_t p, int32_t enable) {
+  if (!p) return fail(DMAS_ERR_NULL, "plan is NULL");
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->timing = enable != 0;
+  return DMAS_OK;
+}
+
+dmas_status dmas_timing_read(dmas_plan_t p, double ms_out[4], int64_t count_out[4]) {
+  if (!p || !ms_out || !count_out) return fail(DMAS_ERR_NULL, "NULL argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard guard(p->device);
+  for (int k = 0; k < 4; ++k) {
+    ms_out[k] = 0.0;
+    count_out[k] = 0;
+  }
+  dmas_status rc = DMAS_OK;
+  for (auto& r : p->recs) {
+    cudaError_t e = cudaEventSynchronize(r.ev1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.ev0, r.ev1);
+    if (e != cudaSuccess && rc == DMAS_OK) rc = fail(DMAS_ERR_CUDA, std::string("timing: ") + cudaGetErrorString(e));
+    ms_out[r.kernel] += ms;
+    count_out[r.kernel] += 1;
+    p->ev_pool.push_back(r.ev0);
+    p->ev_pool.push_back(r.ev1);
+  }
+  p->recs.clear();
+  return rc;
+}
+
+int64_t dmas_launch_count(void) { return g_launches.load(); }
+
+void dmas_destroy(dmas_plan_t p) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    DeviceGuard guard(p->device);
+    cudaDeviceSynchronize();
+    free_plan_memory(p);
+  }
+  delete p;
+}
+
+const char* dmas_status_string(dmas_status s) {
+  switch (s) {
+    case DMAS_OK: return "DMAS_OK";
+    case DMAS_ERR_NULL: return "DMAS_ERR_NULL";
+    case DMAS_ERR_INVALID: return "DMAS_ERR_INVALID";
+    case DMAS_ERR_ORDER: return "DMAS_ERR_ORDER";
+    case DMAS_ERR_SHAPE: return "DMAS_ERR_SHAPE";
+    case DMAS_ERR_CUDA: return "DMAS_ERR_CUDA";
+    case DMAS_ERR_OOM: return "DMAS_ERR_OOM";
+  }
+  return "DMAS_ERR_UNKNOWN";
+}
+
+const char* dmas_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

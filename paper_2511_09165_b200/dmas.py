@@ -1,0 +1,287 @@
+"""Thin ctypes binding of include/dmas.h (argument marshalling only).
+
+Every step of the beamforming path runs in libdmas.so's sm_100a kernels; this module only
+packs descriptors, passes device pointers (torch tensors' ``data_ptr()``) and the current
+CUDA stream, and turns status codes into exceptions.  There is no CPU fallback: if the
+shared library is missing or fails to load, importing this module raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libdmas.so")
+
+KIND_DAS, KIND_DMAS, KIND_CFDMAS, KIND_CFDAS, KIND_CF = 1, 2, 4, 8, 16
+KIND_ALL = 31
+KIND_BITS = {"das": KIND_DAS, "dmas": KIND_DMAS, "cfdmas": KIND_CFDMAS, "cfdas": KIND_CFDAS, "cf": KIND_CF}
+KIND_ORDER = ("das", "dmas", "cfdmas", "cfdas", "cf")     # bit order = order of `outs`
+
+STATUS = {0: "DMAS_OK", 1: "DMAS_ERR_NULL", 2: "DMAS_ERR_INVALID", 3: "DMAS_ERR_ORDER", 4: "DMAS_ERR_SHAPE",
+          5: "DMAS_ERR_CUDA", 6: "DMAS_ERR_OOM"}
+
+
+def RAW(kinds: int) -> int:
+    return int(kinds) & KIND_ALL
+
+
+def ENV(kinds: int) -> int:
+    return (int(kinds) & KIND_ALL) << 8
+
+
+class DmasError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+class dmas_plan_desc(ctypes.Structure):
+    _fields_ = [
+        ("n_mics", ctypes.c_int32),
+        ("mic_xyz", ctypes.POINTER(ctypes.c_double)),
+        ("n_dirs", ctypes.c_int64),
+        ("dir_az_el", ctypes.POINTER(ctypes.c_double)),
+        ("reference_xyz", ctypes.POINTER(ctypes.c_double)),
+        ("fs_hz", ctypes.c_double),
+        ("c_mps", ctypes.c_double),
+        ("order", ctypes.c_int32),
+        ("n_samples", ctypes.c_int64),
+        ("max_frames", ctypes.c_int32),
+        ("cf_eps", ctypes.c_float),
+        ("lp_taps", ctypes.c_int32),
+        ("lp_cutoff_hz", ctypes.c_double),
+        ("bp_taps", ctypes.c_int32),
+        ("bp_coeffs", ctypes.POINTER(ctypes.c_float)),
+        ("env_decim", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("scratch_bytes", ctypes.c_int64),
+    ]
+
+
+class dmas_plan_info(ctypes.Structure):
+    _fields_ = [
+        ("n_dirs", ctypes.c_int64), ("n_samples", ctypes.c_int64), ("n_out_samples", ctypes.c_int64),
+        ("n_mics", ctypes.c_int32), ("order", ctypes.c_int32), ("lp_taps", ctypes.c_int32),
+        ("env_decim", ctypes.c_int32), ("device", ctypes.c_int32), ("d_min", ctypes.c_int32),
+        ("d_max", ctypes.c_int32), ("psi_tile", ctypes.c_int32), ("t_tile", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("chunk_frames", ctypes.c_int32),
+    ]
+
+
+# The exported C symbols (include/dmas.h).  tests/test_abi.py checks the .so exports each.
+EXPORTS = ("dmas_plan_desc_init", "dmas_plan", "dmas_beamform", "dmas_beamform_host", "dmas_delay_table",
+           "dmas_get_plan_info", "dmas_set_timing", "dmas_timing_read", "dmas_launch_count", "dmas_destroy",
+           "dmas_status_string", "dmas_last_error")
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P = ctypes.c_void_p
+    lib.dmas_plan_desc_init.argtypes = [ctypes.POINTER(dmas_plan_desc)]
+    lib.dmas_plan_desc_init.restype = None
+    lib.dmas_plan.argtypes = [ctypes.POINTER(dmas_plan_desc), ctypes.POINTER(P)]
+    lib.dmas_plan.restype = ctypes.c_int
+    lib.dmas_beamform.argtypes = [P, P, ctypes.c_int32, ctypes.POINTER(P), ctypes.c_uint32, P]
+    lib.dmas_beamform.restype = ctypes.c_int
+    lib.dmas_beamform_host.argtypes = [P, P, ctypes.c_int32, ctypes.POINTER(P), ctypes.c_uint32]
+    lib.dmas_beamform_host.restype = ctypes.c_int
+    lib.dmas_delay_table.argtypes = [P, P]
+    lib.dmas_delay_table.restype = ctypes.c_int
+    lib.dmas_get_plan_info.argtypes = [P, ctypes.POINTER(dmas_plan_info)]
+    lib.dmas_get_plan_info.restype = ctypes.c_int
+    lib.dmas_set_timing.argtypes = [P, ctypes.c_int32]
+    lib.dmas_set_timing.restype = ctypes.c_int
+    lib.dmas_timing_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    lib.dmas_timing_read.restype = ctypes.c_int
+    lib.dmas_launch_count.argtypes = []
+    lib.dmas_launch_count.restype = ctypes.c_int64
+    lib.dmas_destroy.argtypes = [P]
+    lib.dmas_destroy.restype = None
+    lib.dmas_status_string.argtypes = [ctypes.c_int]
+    lib.dmas_status_string.restype = ctypes.c_char_p
+    lib.dmas_last_error.argtypes = []
+    lib.dmas_last_error.restype = ctypes.c_char_p
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != 0:
+        raise DmasError(status, lib.dmas_last_error().decode(errors="replace"))
+
+
+def launch_count() -> int:
+    return int(lib.dmas_launch_count())
+
+
+def _f64(a, shape_last):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2 or a.shape[1] != shape_last:
+        raise ValueError(f"expected [n][{shape_last}] array, got {a.shape}")
+    return a
+
+
+def _current_stream_ptr():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Plan:
+    """Owns a ``dmas_plan_t``.  Names and arguments follow include/dmas.h."""
+
+    def __init__(self, mic_xyz, dir_az_el, fs: float, c: float, order: int, n_samples: int, *,
+                 max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
+                 lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
+                 device: int = -1, scratch_bytes: int = 0):
+        self._h = ctypes.c_void_p()
+        self._keep = []
+        mic = _f64(mic_xyz, 3)
+        dirs = _f64(dir_az_el, 2)
+        d = dmas_plan_desc()
+        lib.dmas_plan_desc_init(ctypes.byref(d))
+        d.n_mics = mic.shape[0]
+        d.mic_xyz = mic.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        d.n_dirs = dirs.shape[0]
+        d.dir_az_el = dirs.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        if reference_xyz is not None:
+            ref = np.ascontiguousarray(np.asarray(reference_xyz, dtype=np.float64).reshape(3))
+            self._keep.append(ref)
+            d.reference_xyz = ref.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        d.fs_hz, d.c_mps, d.order, d.n_samples = float(fs), float(c), int(order), int(n_samples)
+        d.max_frames, d.cf_eps, d.lp_taps, d.lp_cutoff_hz = int(max_frames), float(cf_eps), int(lp_taps), float(lp_cutoff_hz)
+        if bp_coeffs is not None and len(bp_coeffs) > 0:
+            bp = np.ascontiguousarray(np.asarray(bp_coeffs, dtype=np.float32))
+            self._keep.append(bp)
+            d.bp_taps = bp.shape[0]
+            d.bp_coeffs = bp.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        d.env_decim, d.device, d.scratch_bytes = int(env_decim), int(device), int(scratch_bytes)
+        self._keep += [mic, dirs]
+        _check(lib.dmas_plan(ctypes.byref(d), ctypes.byref(self._h)))
+        info = dmas_plan_info()
+        _check(lib.dmas_get_plan_info(self._h, ctypes.byref(info)))
+        self.info = {name: getattr(info, name) for name, _ in dmas_plan_info._fields_}
+        self.n_mics, self.n_dirs = int(info.n_mics), int(info.n_dirs)
+        self.n_samples, self.n_out_samples = int(info.n_samples), int(info.n_out_samples)
+        self.order, self.max_frames = int(info.order), int(max_frames)
+        self.device = int(info.device)
+
+    # -- dmas_delay_table
+    def delay_table(self) -> np.ndarray:
+        out = np.empty((self.n_dirs, self.n_mics), dtype=np.int32)
+        _check(lib.dmas_delay_table(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def out_shapes(self, n_frames: int, what: int):
+        raw_k, env_k = what & KIND_ALL, (what >> 8) & KIND_ALL
+        shapes = []
+        for name in KIND_ORDER:
+            if raw_k & KIND_BITS[name]:
+                shapes.append(("raw", name, (n_frames, self.n_dirs, self.n_samples)))
+        for name in KIND_ORDER:
+            if env_k & KIND_BITS[name]:
+                shapes.append(("env", name, (n_frames, self.n_dirs, self.n_out_samples)))
+        return shapes
+
+    # -- dmas_beamform (device buffers, async on the current torch stream)
+    def beamform(self, signals, what: int, outs: Optional[list] = None, stream=None) -> Dict:
+        import torch
+        if not (isinstance(signals, torch.Tensor) and signals.is_cuda and signals.dtype == torch.float32):
+            raise TypeError("signals must be a CUDA float32 tensor [F][n_mics][T]")
+        if not signals.is_contiguous() or signals.dim() != 3 or signals.shape[1:] != (self.n_mics, self.n_samples):
+            raise ValueError(f"signals must be contiguous [F][{self.n_mics}][{self.n_samples}], got {tuple(signals.shape)}")
+        F = signals.shape[0]
+        shapes = self.out_shapes(F, what)
+        if outs is None:
+            outs = [torch.empty(s, dtype=torch.float32, device=signals.device) for (_, _, s) in shapes]
+        if len(outs) != len(shapes):
+            raise ValueError("wrong number of output buffers")
+        for o, (_, _, s) in zip(outs, shapes):
+            if tuple(o.shape) != s or o.dtype != torch.float32 or not o.is_contiguous() or not o.is_cuda:
+                raise ValueError(f"output buffer must be contiguous float32 {s}")
+        arr = (ctypes.c_void_p * max(1, len(outs)))(*[o.data_ptr() for o in outs])
+        st = ctypes.c_void_p(stream) if isinstance(stream, int) else (
+            ctypes.c_void_p(stream.cuda_stream) if stream is not None else _current_stream_ptr())
+        _check(lib.dmas_beamform(self._h, ctypes.c_void_p(signals.data_ptr()), F, arr, what, st))
+        return {(stage, name): o for (stage, name, _), o in zip(shapes, outs)}
+
+    # -- dmas_beamform_host (host buffers, synchronous, pipelined copies)
+    def beamform_host(self, signals: np.ndarray, what: int, outs: Optional[list] = None) -> Dict:
+        if signals.dtype != np.float32 or not signals.flags.c_contiguous:
+            raise TypeError("signals must be C-contiguous float32")
+        if signals.ndim != 3 or signals.shape[1:] != (self.n_mics, self.n_samples):
+            raise ValueError("signals must be [F][n_mics][T]")
+        F = signals.shape[0]
+        shapes = self.out_shapes(F, what)
+        if outs is None:
+            outs = [np.empty(s, dtype=np.float32) for (_, _, s) in shapes]
+        for o, (_, _, s) in zip(outs, shapes):
+            if o.shape != s or o.dtype != np.float32 or not o.flags.c_contiguous:
+                raise ValueError(f"output buffer must be contiguous float32 {s}")
+        arr = (ctypes.c_void_p * max(1, len(outs)))(*[_host_ptr(o) for o in outs])
+        _check(lib.dmas_beamform_host(self._h, ctypes.c_void_p(_host_ptr(signals)), F, arr, what))
+        return {(stage, name): o for (stage, name, _), o in zip(shapes, outs)}
+
+    # -- per-kernel device timing
+    def set_timing(self, enable: bool):
+        _check(lib.dmas_set_timing(self._h, 1 if enable else 0))
+
+    def timing_read(self):
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_int64 * 4)()
+        _check(lib.dmas_timing_read(self._h, ms, cnt))
+        names = ("delay_table", "signed_roots", "beamform", "envelope")
+        return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(names)}
+
+    def close(self):
+        if self._h:
+            lib.dmas_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def _host_ptr(a) -> int:
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()      # pinned torch CPU tensor
+
+
+# C-ABI names (same names as include/dmas.h)
+def dmas_plan(*args, **kw) -> Plan:
+    return Plan(*args, **kw)
+
+
+def dmas_beamform(plan: Plan, signals, what: int, outs=None, stream=None):
+    return plan.beamform(signals, what, outs, stream)
+
+
+def dmas_beamform_host(plan: Plan, signals, what: int, outs=None):
+    return plan.beamform_host(signals, what, outs)
+
+
+def dmas_delay_table(plan: Plan):
+    return plan.delay_table()
+
+
+def dmas_destroy(plan: Plan):
+    plan.close()

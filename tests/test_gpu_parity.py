@@ -1,0 +1,342 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on identical
+seeded inputs.  Bar (BASELINE.json north_star): delay tables bit-exact; every image kind,
+frame and stage within max|gpu - oracle| <= 1e-4 * max|oracle|."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dmas_oracle as O
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4           # relative to the image peak (north_star)
+KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
+
+
+@pytest.fixture(scope="module")
+def dm():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2511_09165_b200 import dmas
+    return dmas
+
+
+def run_gpu(dm, mic, dirs, fs, c, p, signals, what, **kw):
+    import torch
+    F = signals.shape[0]
+    plan = dm.Plan(mic, dirs, fs, c, p, signals.shape[2], max_frames=max(1, F), **kw)
+    x = torch.from_numpy(np.ascontiguousarray(signals)).cuda()
+    res = plan.beamform(x, what)
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy() for k, v in res.items()}
+    return plan, out
+
+
+def oracle_images(mic, dirs, fs, c, p, signals, kinds=KINDS, env_kinds=(), lp_taps=127, cutoff=5000.0,
+                  bp=None, decim=1, d=None, eps=1e-30):
+    if d is None:
+        d = O.delay_table(mic, dirs, fs, c)
+    h = O.lpf_taps(lp_taps, cutoff, fs) if env_kinds else None
+    out = {}
+    for f in range(signals.shape[0]):
+        img = O.beamform_frame(signals[f], d, p, eps=eps)
+        for k in kinds:
+            out.setdefault(("raw", k), []).append(img[k])
+        for k in env_kinds:
+            out.setdefault(("env", k), []).append(O.envelope(img[k], h, bp_taps=bp, decim=decim))
+    return {k: np.stack(v) for k, v in out.items()}
+
+
+def assert_parity(gpu, ref, label="", zero_scale=None):
+    """max|gpu - ref| <= 1e-4 * max|ref| per frame.  When the oracle image is exactly zero the
+    relative criterion is undefined; fp32 Newton-Girard then leaves a rounding residue of the
+    order of the inputs, so the bound is taken relative to `zero_scale` (an upper bound of
+    |image| from the input amplitudes) when given, else 1e-30."""
+    assert gpu.shape == ref.shape, (label, gpu.shape, ref.shape)
+    for f in range(ref.shape[0]):
+        peak = float(np.max(np.abs(ref[f])))
+        err = float(np.max(np.abs(gpu[f].astype(np.float64) - ref[f])))
+        bound = TOL * peak if peak > 0 else (TOL * zero_scale if zero_scale else 1e-30)
+        assert np.all(np.isfinite(gpu[f])), label
+        assert err <= bound, f"{label} frame {f}: max err {err:.3e} > {bound:.3e} (peak {peak:.3e})"
+
+
+def what_all(dm, env=True):
+    return dm.RAW(dm.KIND_ALL) | (dm.ENV(dm.KIND_ALL) if env else 0)
+
+
+# ------------------------------------------------------------------ A1 bit-exact delay tables
+@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C5", "paper3601"])
+def test_delay_table_bitexact(dm, name):
+    if name == "paper3601":          # 3601 azimuths, 0.05 deg, el 0, 32-mic eRTIS-like
+        mic, dirs = gen.disk_array(32, seed=7), gen.az_grid_deg(np.linspace(-90, 90, 3601))
+    elif name == "C4":
+        mic, dirs = gen.disk_array(64, 0.10, 4e-3, seed=11), gen.az_el_grid(128, 90.0, 128, 60.0)
+    elif name == "C5":
+        mic, dirs = gen.disk_array(32, seed=7), gen.az_el_grid(128, 90.0, 128, 60.0)
+    elif name == "C2":
+        mic, dirs = gen.disk_array(32, seed=7), gen.az_el_grid(60, 90.0, 30, 45.0)
+    else:
+        mic, dirs = gen.ula(8), gen.az_grid_deg(np.arange(-90, 91, 2))
+    plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, 2, 64)
+    d_gpu = plan.delay_table()
+    d_ref, v = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, return_exact=True)
+    assert np.array_equal(d_gpu, d_ref)
+    margin = float(np.min(np.abs(np.abs(v - np.floor(v)) - 0.5)))
+    assert margin > 1e-9        # no near-ties: the bit-exact claim is not luck
+    assert plan.info["d_min"] == d_ref.min() and plan.info["d_max"] == d_ref.max()
+
+
+def test_delay_table_reference_point_and_ties(dm):
+    mics = np.array([[-0.5, 0, 0], [-1.5, 0, 0], [-2.5, 0, 0], [0.5, 0, 0], [-2.4, 0.1, 0], [-2.6, 0, 0.1]])
+    plan = dm.Plan(mics, [[0.0, 0.0]], 343.0, 343.0, 2, 16, lp_taps=0)
+    assert plan.delay_table().tolist() == O.delay_table(mics, [[0.0, 0.0]], 343.0, 343.0).tolist()
+    mic = gen.disk_array(16, seed=3)
+    dirs = gen.az_el_grid(9, 80.0, 7, 50.0)
+    ref = np.array([0.01, -0.02, 0.005])
+    plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, 2, 16, reference_xyz=ref)
+    assert np.array_equal(plan.delay_table(), O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, reference=ref))
+
+
+# ------------------------------------------------------------------ slice harness (broadside, zero delays)
+def _slice_plan(dm, n, p, T):
+    mic = np.stack([np.zeros(n), 0.003 * np.arange(n) - 0.0015 * (n - 1), np.zeros(n)], axis=1)
+    return dm.Plan(mic, [[0.0, 0.0]], gen.FS, gen.C_SOUND, p, T)
+
+
+def test_slice_harness_worked_examples(dm, golden):
+    """Array in the y-z plane + one broadside direction => every delay is 0 and x_i(t) = m_i[t]:
+    each sample column is an independent slice.  SPEC worked examples on the GPU."""
+    import torch
+    cases = [(np.array([1, 4, 9.0]), 2, {"dmas": 11.0, "das": 14.0}),
+             (np.array([1, 8, 27, 64.0]), 3, {"dmas": 50.0, "das": 100.0}),
+             (np.array([1, 0, 0, 0.0]), 2, {"cf": 0.25}),
+             (np.array([1, -1.0]), 2, {"cf": 0.0, "dmas": -1.0})]
+    for x, p, exp in cases:
+        plan = _slice_plan(dm, len(x), p, 1)
+        assert np.all(plan.delay_table() == 0)
+        sig = torch.tensor(x, dtype=torch.float32).reshape(1, len(x), 1).cuda()
+        res = plan.beamform(sig, dm.RAW(dm.KIND_ALL))
+        for k, v in exp.items():
+            assert float(res[("raw", k)].item()) == pytest.approx(v, rel=1e-6, abs=1e-6), (x, p, k)
+
+
+def test_slice_harness_random_bruteforce(dm):
+    """Random slices (N <= 10, p <= 5) against Eq. (5) brute force, plus S(lam x) = lam S(x)
+    and S(-x) = (-1)^p S(x) on the GPU."""
+    import torch
+    rng = np.random.default_rng(21)
+    for p in (2, 3, 4, 5):
+        for n in (p, 7, 10):
+            T = 300
+            x = rng.uniform(-1, 1, (n, T)).astype(np.float32)
+            plan = _slice_plan(dm, n, p, T)
+            sig = torch.from_numpy(x[None]).cuda()
+            g = plan.beamform(sig, dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
+            g2 = plan.beamform(2.0 * sig, dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
+            gn = plan.beamform(-sig, dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
+            ref = np.array([O.brute_force_esp(list(O.signed_root(x[:, t].astype(np.float64), p)), p)
+                            for t in range(T)])
+            peak = np.max(np.abs(ref))
+            assert np.max(np.abs(g - ref)) <= 1e-5 * peak
+            assert np.max(np.abs(g2 - 2 * ref)) <= 1e-5 * 2 * peak
+            assert np.max(np.abs(gn - (-1) ** p * ref)) <= 1e-5 * peak
+
+
+# ------------------------------------------------------------------ random multi-tile / ragged cases
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_random_multi_tile_all_kinds(dm, p):
+    """Several psi tiles (70 dirs = 2 full + ragged), several t tiles (700 = 2 full + ragged),
+    3 frames, 11 mics, every kind, raw + envelope."""
+    mic = gen.disk_array(11, 0.08, 5e-3, seed=30 + p)
+    dirs = gen.az_el_grid(10, 80.0, 7, 50.0)
+    sig = gen.random_signals(3, 11, 700, seed=40 + p, sparsity=0.1)
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, p, sig, what_all(dm))
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
+    for key in ref:
+        assert_parity(g[key], ref[key], f"p={p} {key}")
+
+
+# ------------------------------------------------------------------ BASELINE.json configs
+def _config_parity(dm, name, p=None, env=True):
+    cfg = gen.config(name)
+    p = p or cfg["order"]
+    plan, g = run_gpu(dm, cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, cfg["signals"], what_all(dm, env))
+    ref = oracle_images(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, cfg["signals"],
+                        env_kinds=KINDS if env else ())
+    for key in ref:
+        assert_parity(g[key], ref[key], f"{name} p={p} {key}")
+
+
+def test_config_C1(dm):
+    _config_parity(dm, "C1")
+
+
+def test_config_C2(dm):
+    _config_parity(dm, "C2")
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_config_C3_order_sweep(dm, p):
+    _config_parity(dm, "C3", p=p)
+
+
+def _sampled_rows(dm, cfg, p, what, frames_idx, n_rows, seed, **kw):
+    """Full-size GPU run; oracle on sampled (frame, direction) rows (rows are independent)."""
+    import torch
+    sig = cfg["signals"]
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, cfg["T"], max_frames=sig.shape[0], **kw)
+    x = torch.from_numpy(sig).cuda()
+    res = plan.beamform(x, what)
+    torch.cuda.synchronize()
+    d = plan.delay_table()
+    assert np.array_equal(d, O.delay_table(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"]))
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(len(cfg["dirs"]), n_rows, replace=False))
+    env_k = [k for k in KINDS if (what >> 8) & dm.KIND_BITS[k]]
+    raw_k = [k for k in KINDS if what & dm.KIND_BITS[k]]
+    h = O.lpf_taps()
+    for f in frames_idx:
+        img = O.beamform_frame(sig[f], d[rows], p)
+        for k in raw_k:
+            assert_parity(res[("raw", k)][f][rows].cpu().numpy()[None], img[k][None], f"{cfg['name']} raw {k} f{f}")
+        for k in env_k:
+            assert_parity(res[("env", k)][f][rows].cpu().numpy()[None], O.envelope(img[k], h)[None],
+                          f"{cfg['name']} env {k} f{f}")
+    return res
+
+
+def test_config_C4_sampled(dm):
+    cfg = gen.config("C4")
+    _sampled_rows(dm, cfg, 3, dm.RAW(dm.KIND_DAS | dm.KIND_DMAS | dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS),
+                  [0], 96, seed=1)
+
+
+def test_config_C5_bench_launch_sampled(dm):
+    """C5 in the launch configuration bench.py times (256 frames, CF-DMAS2 envelope only,
+    internal frame chunks through the plan scratch); sampled frames {0, 128, 255}."""
+    cfg = gen.config("C5")
+    _sampled_rows(dm, cfg, 2, dm.ENV(dm.KIND_CFDMAS), [0, 128, 255], 48, seed=2)
+
+
+# ------------------------------------------------------------------ edge cases and variants
+def test_edge_shapes(dm):
+    import torch
+    rng = np.random.default_rng(50)
+    # T = 1, one direction, n_mics == p
+    for (n, p, T, nd) in [(2, 2, 1, 1), (5, 5, 3, 2), (3, 3, 33, 1)]:
+        mic = gen.disk_array(n, 0.05, 5e-3, seed=n)
+        dirs = gen.az_el_grid(nd, 30.0, 1, 0.0) if nd > 1 else np.array([[0.2, 0.1]])
+        sig = rng.standard_normal((2, n, T)).astype(np.float32)
+        plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, p, sig, what_all(dm))
+        ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
+        # |E_p| <= C(N,p) max|x| and |A| <= N max|x|: the amplitude scale of every kind
+        scale = math.comb(n, p) * float(np.max(np.abs(sig))) + n * float(np.max(np.abs(sig)))
+        for key in ref:
+            assert_parity(g[key], ref[key], f"edge n={n} p={p} T={T} {key}", zero_scale=scale)
+    # n_frames == 0 is a no-op
+    plan = dm.Plan(gen.ula(4), gen.az_grid_deg([0, 10]), gen.FS, gen.C_SOUND, 2, 16, max_frames=2)
+    res = plan.beamform(torch.zeros((0, 4, 16), device="cuda"), dm.RAW(dm.KIND_DAS))
+    assert res[("raw", "das")].shape == (0, 2, 16)
+    # all-zero input -> all-zero images (CF guarded by eps)
+    res = plan.beamform(torch.zeros((2, 4, 16), device="cuda"), what_all(dm))
+    for v in res.values():
+        assert float(v.abs().max()) == 0.0
+    # too many frames
+    with pytest.raises(dm.DmasError):
+        plan.beamform(torch.zeros((3, 4, 16), device="cuda"), dm.RAW(dm.KIND_DAS))
+
+
+def test_short_frames_mostly_out_of_range(dm):
+    """T = 16 with delays up to +-65: most gathered samples fall outside [0, T) and read 0."""
+    mic = gen.disk_array(32, seed=7)
+    dirs = gen.az_el_grid(6, 90.0, 5, 60.0)
+    sig = gen.random_signals(2, 32, 16, seed=51)
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, 3, sig, what_all(dm))
+    assert plan.info["d_max"] > 16
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, 3, sig, env_kinds=KINDS)
+    for key in ref:
+        assert_parity(g[key], ref[key], f"short {key}")
+
+
+def test_generic_envelope_bandpass_decimation(dm):
+    """Generic K4 path: 63-tap low-pass at 8 kHz, a 31-tap band-pass, decimation R = 3."""
+    import scipy.signal as ss
+    bp = ss.firwin(31, [20e3, 60e3], pass_zero=False, fs=gen.FS).astype(np.float32)
+    mic = gen.disk_array(16, seed=5)
+    dirs = gen.az_el_grid(5, 60.0, 8, 30.0)
+    sig = gen.random_signals(2, 16, 1000, seed=52)
+    for kw, okw in [(dict(lp_taps=63, lp_cutoff_hz=8000.0, env_decim=3, bp_coeffs=bp),
+                     dict(lp_taps=63, cutoff=8000.0, decim=3, bp=bp.astype(np.float64))),
+                    (dict(env_decim=4), dict(decim=4)),
+                    (dict(bp_coeffs=bp), dict(bp=bp.astype(np.float64)))]:
+        plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, 2, sig, dm.ENV(dm.KIND_DAS | dm.KIND_CFDMAS), **kw)
+        ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, 2, sig, kinds=(), env_kinds=("das", "cfdmas"), **okw)
+        for key in ref:
+            assert_parity(g[key], ref[key], f"generic {kw.keys()} {key}")
+
+
+def test_cf_eps_zero_nonzero_input(dm):
+    mic = gen.disk_array(8, seed=6)
+    dirs = gen.az_el_grid(4, 40.0, 4, 20.0)
+    sig = gen.random_signals(1, 8, 300, seed=53)
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, 2, sig, dm.RAW(dm.KIND_CF | dm.KIND_CFDMAS), cf_eps=0.0)
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, 2, sig, kinds=("cf", "cfdmas"), eps=0.0)
+    assert_parity(g[("raw", "cf")], ref[("raw", "cf")], "cf eps 0")
+    assert float(np.max(g[("raw", "cf")])) <= 1.0 + 1e-5
+
+
+# ------------------------------------------------------------------ runtime invariances (bitwise)
+def test_host_pipeline_matches_device_bitwise(dm):
+    import torch
+    cfg = gen.config("C5", frames=5)
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"][:2000], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=2)
+    what = dm.RAW(dm.KIND_DAS) | dm.ENV(dm.KIND_CFDMAS)
+    host = plan.beamform_host(cfg["signals"], what)                # 5 frames through 2-frame stages
+    for f0 in range(0, 5, 2):
+        x = torch.from_numpy(cfg["signals"][f0:f0 + 2]).cuda()
+        dev = plan.beamform(x, what)
+        torch.cuda.synchronize()
+        for k in dev:
+            assert np.array_equal(dev[k].cpu().numpy(), host[k][f0:f0 + 2]), k
+
+
+def test_chunking_and_sharding_bitwise(dm):
+    """Frame chunking (tiny scratch budget -> 1 frame per chunk) and direction sharding (G = 1
+    vs 2 / 3 contiguous slices, SPEC.md:323 'bitwise independent of the partitioning') do not
+    change a single bit."""
+    import torch
+    cfg = gen.config("C3")
+    sig = np.concatenate([cfg["signals"], gen.random_signals(2, 32, cfg["T"], seed=54)])
+    what = dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS | dm.KIND_DAS)
+    x = torch.from_numpy(sig).cuda()
+    full = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 4, cfg["T"], max_frames=3)
+    a = {k: v.cpu().numpy() for k, v in full.beamform(x, what).items()}
+    small = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 4, cfg["T"], max_frames=3, scratch_bytes=1)
+    b = {k: v.cpu().numpy() for k, v in small.beamform(x, what).items()}
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    nd = len(cfg["dirs"])
+    for G in (2, 3):
+        bounds = np.linspace(0, nd, G + 1).astype(int)
+        for g0, g1 in zip(bounds[:-1], bounds[1:]):
+            sh = dm.Plan(cfg["mic_xyz"], cfg["dirs"][g0:g1], cfg["fs"], cfg["c"], 4, cfg["T"], max_frames=3)
+            r = sh.beamform(x, what)
+            for k in a:
+                assert np.array_equal(a[k][:, g0:g1], r[k].cpu().numpy()), (G, k)
+
+
+def test_timing_and_launch_counter(dm):
+    import torch
+    plan = dm.Plan(gen.ula(8), gen.az_grid_deg(np.arange(-90, 91, 2)), gen.FS, gen.C_SOUND, 2, 1024, max_frames=4)
+    x = torch.from_numpy(gen.random_signals(4, 8, 1024, seed=55)).cuda()
+    n0 = dm.launch_count()
+    plan.set_timing(True)
+    plan.beamform(x, dm.ENV(dm.KIND_CFDMAS))
+    t = plan.timing_read()
+    assert dm.launch_count() - n0 == 3
+    assert t["beamform"][1] == 1 and t["envelope"][1] == 1 and t["signed_roots"][1] == 1
+    assert all(ms > 0 for ms, c in t.values() if c)

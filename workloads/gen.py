@@ -124,11 +124,12 @@ def random_reflectors(n: int, dirs, r_lo: float, r_hi: float, a_lo: float, a_hi:
 
 
 # ------------------------------------------------------------------ configs (BASELINE.json "configs")
-def config(name: str, frames=None):
+def config(name: str, frames=None, stream: int = 0):
     """Scene + plan parameters of BASELINE.json configs C1..C5.
 
     Returns dict: mic_xyz, dirs, fs, c, order, T, signals fp32 [F][n_mics][T], plus
-    metadata.  ``frames`` overrides the frame count (C5 only)."""
+    metadata.  ``frames`` overrides the frame count (C5 only); ``stream`` selects an
+    independent C5 frame stream (other reflectors and noise; used per rank in bench.py)."""
     if name == "C1":
         mic = ula(8)
         dirs = az_grid_deg(np.arange(-90, 91, 2))
@@ -158,11 +159,11 @@ def config(name: str, frames=None):
         dirs = az_el_grid(128, 90.0, 128, 60.0)
         T, p = 4096, 2
         F = 256 if frames is None else int(frames)
-        base = random_reflectors(3, dirs, 0.3, 1.0, 0.3, 1.0, seed=5)
+        base = random_reflectors(3, dirs, 0.3, 1.0, 0.3, 1.0, seed=5 + 7919 * stream)
         sig = np.empty((F, mic.shape[0], T), dtype=np.float32)
         for f in range(F):
             refl = [(az, el, R + 1e-3 * f, a) for (az, el, R, a) in base]
-            sig[f] = frame(mic, refl, T, snr_db=10.0, seed=5 + f)
+            sig[f] = frame(mic, refl, T, snr_db=10.0, seed=5 + f + 1_000_003 * stream)
     else:
         raise KeyError(name)
     return dict(name=name, mic_xyz=mic, dirs=dirs, fs=FS, c=C_SOUND, order=p, T=T,
