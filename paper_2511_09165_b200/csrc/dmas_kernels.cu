@@ -192,8 +192,16 @@ template <> __device__ __forceinline__ void acc_final<5>(const Acc<5>& c, float&
        30.f * P1 * P4 + 24.f * P5) * (1.f / 120.f);
 }
 
-template <int P>
-__global__ void __launch_bounds__(BF_THREADS, 2) k_beamform(const BeamformArgs a) {
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
+// minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
+template <int P, int KM>
+__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? 3 : 2)) k_beamform(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;
@@ -205,6 +213,7 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform(const BeamformArgs a
   const int64_t f = blockIdx.z;
   const int npsi = (int)min((int64_t)BF_PSI, a.n_dirs - psi0);
   const int32_t lo = __ldg(a.tile_lo + blockIdx.y);   // window origin relative to t0 (<= min delay of tile)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -218,15 +227,15 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform(const BeamformArgs a
     for (int i = 0; i < n_mics; ++i) bulk_g2s(win + (size_t)i * W, src + (int64_t)i * a.Tp, row_bytes, &bar);
   }
   // delay rows of this psi tile -> smem word offsets into the window (overlaps the TMA)
-  for (int idx = threadIdx.x; idx < npsi * n_mics; idx += BF_THREADS) {
-    const int q = idx / n_mics, i = idx - q * n_mics;
-    offs[idx] = i * W + (__ldg(a.delays + (psi0 + q) * n_mics + i) - lo);
+  for (int q = warp; q < npsi; q += BF_WARPS) {
+    const int32_t* drow = a.delays + (psi0 + q) * n_mics;
+    for (int i = lane; i < n_mics; i += 32) offs[q * n_mics + i] = i * W + (__ldg(drow + i) - lo);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* wl = win + lane;
+  const bool full_t = t0 + BF_T <= a.T;
   for (int q = warp; q < npsi; q += BF_WARPS) {
     Acc<P> acc[BF_KT];
 #pragma unroll
@@ -238,21 +247,22 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform(const BeamformArgs a
 #pragma unroll
       for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
     }
-    const int64_t psi = psi0 + q;
-    const int64_t rowoff = (f * a.n_dirs + psi) * a.T;
+    const int64_t o = (f * a.n_dirs + psi0 + q) * a.T + t0 + lane;
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) {
-      const int64_t t = t0 + lane + 32 * k;
-      if (t >= a.T) continue;
+      if (!full_t && t0 + lane + 32 * k >= a.T) continue;
       float A, B, E;
       acc_final<P>(acc[k], A, B, E);
-      const float cf = __fdividef(A * A, fmaf(a.n_mics_f, B, a.cf_eps));
-      const int64_t o = rowoff + t;
-      if (a.out[0]) a.out[0][o] = A;
-      if (a.out[1]) a.out[1][o] = E;
-      if (a.out[2]) a.out[2][o] = E * cf;
-      if (a.out[3]) a.out[3][o] = A * cf;
-      if (a.out[4]) a.out[4][o] = cf;
+      const float cf = A * A * rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps));
+      if (KM == 4) {
+        a.out[2][o + 32 * k] = E * cf;
+      } else {
+        if (a.out[0]) a.out[0][o + 32 * k] = A;
+        if (a.out[1]) a.out[1][o + 32 * k] = E;
+        if (a.out[2]) a.out[2][o + 32 * k] = E * cf;
+        if (a.out[3]) a.out[3][o + 32 * k] = A * cf;
+        if (a.out[4]) a.out[4][o + 32 * k] = cf;
+      }
     }
   }
 }
@@ -261,13 +271,27 @@ size_t beamform_smem_bytes(int32_t n_mics, int32_t W) {
   return (size_t)n_mics * W * sizeof(float) + (size_t)BF_PSI * n_mics * sizeof(int32_t);
 }
 
+template <int P>
+static cudaError_t configure_order(int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(k_beamform<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_beamform<P, 31>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 cudaError_t beamform_configure(int32_t n_mics, int32_t W) {
   const int bytes = (int)beamform_smem_bytes(n_mics, W);
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_beamform<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if ((e = configure_order<2>(bytes))) return e;
+  if ((e = configure_order<3>(bytes))) return e;
+  if ((e = configure_order<4>(bytes))) return e;
+  return configure_order<5>(bytes);
+}
+
+template <int P>
+static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
+  if (only_cfdmas) k_beamform<P, 4><<<grid, BF_THREADS, smem, st>>>(a);
+  else k_beamform<P, 31><<<grid, BF_THREADS, smem, st>>>(a);
 }
 
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
@@ -276,59 +300,92 @@ cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, 
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
   const size_t smem = beamform_smem_bytes(a.n_mics, a.W);
   switch (order) {
-    case 2: k_beamform<2><<<grid, BF_THREADS, smem, st>>>(a); break;
-    case 3: k_beamform<3><<<grid, BF_THREADS, smem, st>>>(a); break;
-    case 4: k_beamform<4><<<grid, BF_THREADS, smem, st>>>(a); break;
-    case 5: k_beamform<5><<<grid, BF_THREADS, smem, st>>>(a); break;
+    case 2: launch_order<2>(a, grid, smem, st); break;
+    case 3: launch_order<3>(a, grid, smem, st); break;
+    case 4: launch_order<4>(a, grid, smem, st); break;
+    case 5: launch_order<5>(a, grid, smem, st); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------
-// K4 fast path — 127-tap low-pass of |y|, R = 1, no band-pass.  Each thread produces 4
-// consecutive outputs from 33 float4 smem reads (130 distinct inputs); the taps live in the
-// kernel-parameter constant bank, so every MAC is one FFMA R, R, c[], R.
+// K4 fast path — 127-tap low-pass of |y|, R = 1, no band-pass, T % 4 == 0.  A CTA owns one
+// 1024-sample column tile of ENV_RPC consecutive rows; each row's window [t0 - 64, t0 + 1088)
+// is staged with 16-byte cp.async (zero-fill outside [0, T)), double-buffered so the next row
+// loads while this one computes.  Each thread produces 4 consecutive outputs from 33
+// conflict-free LDS.128; the taps live in the kernel-parameter constant bank and |.| is the
+// free operand modifier, so every MAC is one FFMA R, |R|, c[], R.
 //   e[t] = max(0, sum_k h[k] |y[t + 63 - k]|), zeros outside [0, T)
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __global__ void __launch_bounds__(ENV_THREADS) k_envelope_lp127(const float* __restrict__ y, float* __restrict__ out,
-                                                               int64_t T, const __grid_constant__ LpTaps127 taps) {
-  __shared__ __align__(16) float sa[ENV_T + 128];
-  const int64_t row = blockIdx.x;
+                                                               int64_t rows, int64_t T,
+                                                               const __grid_constant__ LpTaps127 taps) {
+  constexpr int WIN = ENV_T + 128;                     // staged samples per row
+  __shared__ __align__(16) float sa[2][WIN];
   const int64_t t0 = (int64_t)blockIdx.y * ENV_T;
-  const float* yr = y + row * T;
-  for (int u = threadIdx.x; u < ENV_T + 128; u += ENV_THREADS) {
-    const int64_t t = t0 - 64 + u;                     // sa[u] = |y[t0 - 64 + u]|
-    sa[u] = (t >= 0 && t < T) ? fabsf(__ldg(yr + t)) : 0.f;
-  }
-  __syncthreads();
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  const float4* a4 = reinterpret_cast<const float4*>(sa) + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * ENV_RPC;
+  const int nr = (int)min((int64_t)ENV_RPC, rows - r0);
+
+  auto stage = [&](int j, int buf) {                   // sa[buf][u] = y[r0 + j][t0 - 64 + u]
+    const float* yr = y + (r0 + j) * T;
+    for (int c = threadIdx.x; c < WIN / 4; c += ENV_THREADS) {
+      const int64_t t = t0 - 64 + 4 * c;
+      const bool in = (t >= 0) && (t + 4 <= T);        // T % 4 == 0: a chunk is fully in or out
+      cp_async_16(&sa[buf][4 * c], in ? yr + t : yr, in ? 16 : 0);
+    }
+    cp_async_commit();
+  };
+
+  stage(0, 0);
+  const int64_t tb = t0 + 4 * threadIdx.x;
+  for (int j = 0; j < nr; ++j) {
+    if (j + 1 < nr) stage(j + 1, (j + 1) & 1);
+    else cp_async_commit();                            // empty group keeps the wait count uniform
+    cp_async_wait<1>();
+    __syncthreads();
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const float4* a4 = reinterpret_cast<const float4*>(sa[j & 1]) + threadIdx.x;
 #pragma unroll
-  for (int v = 0; v < 33; ++v) {
-    const float4 q = a4[v];
-    const float e[4] = {q.x, q.y, q.z, q.w};
+    for (int v = 0; v < 33; ++v) {
+      const float4 q = a4[v];
+      const float e[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int u = 4 * v + c;                         // sample t0 + 4 tid - 64 + u
+      for (int c = 0; c < 4; ++c) {
+        const int u = 4 * v + c;                       // sample t0 + 4 tid - 64 + u
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int k = j + 127 - u;                     // output t0 + 4 tid + j uses tap k
-        if (k >= 0 && k < ENV_FAST_TAPS) acc[j] = fmaf(taps.h[k], e[c], acc[j]);
+        for (int jj = 0; jj < 4; ++jj) {
+          const int k = jj + 127 - u;                  // output t0 + 4 tid + jj uses tap k
+          if (k >= 0 && k < ENV_FAST_TAPS) acc[jj] = fmaf(taps.h[k], fabsf(e[c]), acc[jj]);
+        }
       }
     }
-  }
-  const int64_t tb = t0 + 4 * threadIdx.x;
-  float* orow = out + row * T;
+    float* orow = out + (r0 + j) * T;
+    if (tb + 4 <= T) {
+      *reinterpret_cast<float4*>(orow + tb) =
+          make_float4(fmaxf(acc[0], 0.f), fmaxf(acc[1], 0.f), fmaxf(acc[2], 0.f), fmaxf(acc[3], 0.f));
+    } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (tb + j < T) orow[tb + j] = fmaxf(acc[j], 0.f);
+      for (int jj = 0; jj < 4; ++jj)
+        if (tb + jj < T) orow[tb + jj] = fmaxf(acc[jj], 0.f);
+    }
+    __syncthreads();                                   // buffer j & 1 is restaged at j + 2
+  }
 }
 
 cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
                                   cudaStream_t st) {
-  dim3 grid((unsigned)rows, (unsigned)((T + ENV_T - 1) / ENV_T));
-  k_envelope_lp127<<<grid, ENV_THREADS, 0, st>>>(y, out, T, taps);
+  dim3 grid((unsigned)((rows + ENV_RPC - 1) / ENV_RPC), (unsigned)((T + ENV_T - 1) / ENV_T));
+  k_envelope_lp127<<<grid, ENV_THREADS, 0, st>>>(y, out, rows, T, taps);
   return cudaGetLastError();
 }
 

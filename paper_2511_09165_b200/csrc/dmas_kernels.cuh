@@ -18,6 +18,7 @@ constexpr int BF_PSI = 32;
 constexpr int ENV_THREADS = 256;
 constexpr int ENV_T = 1024;
 constexpr int ENV_FAST_TAPS = 127;
+constexpr int ENV_RPC = 8;              // rows per CTA (double-buffered staging)
 constexpr int ENV_GEN_T = 256;          // generic path: outputs per CTA
 
 constexpr int N_KINDS = 5;              // DAS, DMAS, CFDMAS, CFDAS, CF (dmas.h bit order)

@@ -246,7 +246,8 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
     if (!((env_kinds >> k) & 1u)) continue;
     const float* y = raw_dst[k];
     float* o = env_dst[k];
-    if (p->lp_fast) {
+    const bool aligned16 = ((uintptr_t)y % 16 == 0) && ((uintptr_t)o % 16 == 0);
+    if (p->lp_fast && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, st, [&] { return dmas::launch_envelope_lp127(y, o, rows, p->T, p->lp127, st); }));
     } else {
       CUDA_TRY(timed(p, K_ENVELOPE, st, [&] {
@@ -470,7 +471,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       PLAN_TRY(cudaMalloc(&p->d_bp, p->h_bp.size() * sizeof(float)));
       PLAN_TRY(cudaMemcpy(p->d_bp, p->h_bp.data(), p->h_bp.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
-    p->lp_fast = (p->lp_taps == dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1);
+    p->lp_fast = (p->lp_taps == dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 && p->T % 4 == 0);
     if (p->lp_fast)
       for (int i = 0; i < dmas::ENV_FAST_TAPS; ++i) p->lp127.h[i] = p->h_lp[i];
   }
