@@ -84,6 +84,11 @@ typedef struct {
   int32_t bp_taps;           /* optional band-pass FIR length (odd); 0 = off (default)           */
   const float* bp_coeffs;    /* [bp_taps] host, copied; applied before |.| as a centred FIR      */
   int32_t env_decim;         /* R >= 1: envelope keeps samples t = 0, R, 2R, ... (ceil(T/R))     */
+  int32_t env_engine;        /* 0 = auto: tensor-core (tcgen05) low-pass with a 3-pass BF16 split
+                                (error <= ~1.1e-5 of the envelope) when lp_taps <= 127, no
+                                band-pass, R == 1 and T % 4 == 0, else the FP32 FIR;
+                                1 = always the FP32 FIR; 2 = tensor cores with a 3-pass TF32
+                                split (~5e-7, twice the MMAs) under the same conditions          */
   /* Runtime. */
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an

@@ -11,7 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdmas.so")
-SOURCES = [os.path.join(CSRC, "dmas_kernels.cu"), os.path.join(CSRC, "dmas_plan.cpp")]
+SOURCES = [os.path.join(CSRC, "dmas_kernels.cu"), os.path.join(CSRC, "dmas_envelope_tc.cu"),
+           os.path.join(CSRC, "dmas_plan.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "dmas_kernels.cuh"), os.path.join(ROOT, "include", "dmas.h")]
 
 

@@ -201,7 +201,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
 template <int P, int KM>
-__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? 3 : 2)) k_beamform(const BeamformArgs a) {
+__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : 2)) k_beamform(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? 3 : 2)) k_beamform(const
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
     const int32_t* oq = offs + q * n_mics;
-#pragma unroll 2
+#pragma unroll BF_UNROLL
     for (int i = 0; i < n_mics; ++i) {
       const float* w = wl + oq[i];
 #pragma unroll

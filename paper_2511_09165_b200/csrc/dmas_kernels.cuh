@@ -8,11 +8,24 @@
 namespace dmas {
 
 // Beamform CTA tile (K3): BF_PSI directions x BF_T samples; 8 warps, lanes over t, 8 t / lane.
+#ifndef DMAS_BF_KT
+#define DMAS_BF_KT 8
+#endif
+#ifndef DMAS_BF_PSI
+#define DMAS_BF_PSI 32
+#endif
+#ifndef DMAS_BF_UNROLL
+#define DMAS_BF_UNROLL 2
+#endif
+#ifndef DMAS_BF_MINB2
+#define DMAS_BF_MINB2 3
+#endif
 constexpr int BF_THREADS = 256;
 constexpr int BF_WARPS = BF_THREADS / 32;
-constexpr int BF_T = 256;
-constexpr int BF_KT = BF_T / 32;
-constexpr int BF_PSI = 32;
+constexpr int BF_KT = DMAS_BF_KT;
+constexpr int BF_T = 32 * BF_KT;
+constexpr int BF_PSI = DMAS_BF_PSI;
+constexpr int BF_UNROLL = DMAS_BF_UNROLL;
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
 constexpr int ENV_THREADS = 256;
@@ -52,6 +65,11 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W);   // opt-in to > 48 K
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).
 cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
                                   cudaStream_t st);
+// K4 tensor-core path (dmas_envelope_tc.cu): odd L <= 127, R = 1, no band-pass, T % 4 == 0,
+// 16-byte aligned rows.  Persistent: one CTA per SM.
+cudaError_t envelope_tc_configure();
+cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
+                               bool bf16, int sm_count, cudaStream_t st);
 cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out,
                                     int32_t decim, const float* lp, int32_t L, const float* bp, int32_t Lb,
                                     cudaStream_t st);

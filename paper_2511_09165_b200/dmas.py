@@ -15,7 +15,7 @@ from typing import Dict, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libdmas.so")
+_LIB_PATH = os.environ.get("DMAS_LIBRARY") or os.path.join(_PKG, "libdmas.so")   # override: experiments only
 
 KIND_DAS, KIND_DMAS, KIND_CFDMAS, KIND_CFDAS, KIND_CF = 1, 2, 4, 8, 16
 KIND_ALL = 31
@@ -58,6 +58,7 @@ class dmas_plan_desc(ctypes.Structure):
         ("bp_taps", ctypes.c_int32),
         ("bp_coeffs", ctypes.POINTER(ctypes.c_float)),
         ("env_decim", ctypes.c_int32),
+        ("env_engine", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
     ]
@@ -142,7 +143,7 @@ class Plan:
     def __init__(self, mic_xyz, dir_az_el, fs: float, c: float, order: int, n_samples: int, *,
                  max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
-                 device: int = -1, scratch_bytes: int = 0):
+                 device: int = -1, scratch_bytes: int = 0, env_engine: int = 0):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -165,6 +166,7 @@ class Plan:
             d.bp_taps = bp.shape[0]
             d.bp_coeffs = bp.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         d.env_decim, d.device, d.scratch_bytes = int(env_decim), int(device), int(scratch_bytes)
+        d.env_engine = int(env_engine)
         self._keep += [mic, dirs]
         _check(lib.dmas_plan(ctypes.byref(d), ctypes.byref(self._h)))
         info = dmas_plan_info()

@@ -340,3 +340,20 @@ def test_timing_and_launch_counter(dm):
     assert dm.launch_count() - n0 == 3
     assert t["beamform"][1] == 1 and t["envelope"][1] == 1 and t["signed_roots"][1] == 1
     assert all(ms > 0 for ms, c in t.values() if c)
+
+
+@pytest.mark.parametrize("engine", [0, 1, 2])
+@pytest.mark.parametrize("T,L", [(4096, 127), (4132, 127), (8192, 127), (256, 63), (700, 1), (4, 127)])
+def test_envelope_engines(dm, engine, T, L):
+    """Envelope through the tensor-core low-pass (engine 0: tcgen05 with a 3-pass BF16 split;
+    engine 2: 3-pass TF32 split; 4096-sample tiles, ragged last tile) and the FP32 FIR (engine 1),
+    each against the oracle."""
+    mic = gen.disk_array(8, 0.05, 5e-3, seed=60)
+    dirs = gen.az_el_grid(9, 60.0, 3, 20.0)
+    sig = gen.random_signals(2, 8, T, seed=61 + T, sparsity=0.2)
+    what = dm.ENV(dm.KIND_CFDMAS | dm.KIND_DAS) | dm.RAW(dm.KIND_DAS)
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, 2, sig, what, lp_taps=L, env_engine=engine)
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, 2, sig, kinds=("das",), env_kinds=("das", "cfdmas"),
+                        lp_taps=L)
+    for key in ref:
+        assert_parity(g[key], ref[key], f"engine={engine} T={T} L={L} {key}")
