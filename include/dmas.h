@@ -86,9 +86,8 @@ typedef struct {
   int32_t env_decim;         /* R >= 1: envelope keeps samples t = 0, R, 2R, ... (ceil(T/R))     */
   int32_t env_engine;        /* 0 = auto: tensor-core (tcgen05) low-pass with a 3-pass BF16 split
                                 (error <= ~1.1e-5 of the envelope) when lp_taps <= 127, no
-                                band-pass, R == 1 and T % 4 == 0, else the FP32 FIR;
-                                1 = always the FP32 FIR; 2 = tensor cores with a 3-pass TF32
-                                split (~5e-7, twice the MMAs) under the same conditions          */
+                                band-pass, R == 1, T % 32 == 0 and 16-byte aligned buffers,
+                                else the FP32 FIR; 1 = always the FP32 FIR                      */
   /* Runtime. */
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an

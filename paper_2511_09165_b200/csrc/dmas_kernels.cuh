@@ -65,11 +65,12 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W);   // opt-in to > 48 K
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).
 cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
                                   cudaStream_t st);
-// K4 tensor-core path (dmas_envelope_tc.cu): odd L <= 127, R = 1, no band-pass, T % 4 == 0,
-// 16-byte aligned rows.  Persistent: one CTA per SM.
+// K4 tensor-core path (dmas_envelope_tc.cu): odd L <= 127, R = 1, no band-pass, T % 32 == 0,
+// 16-byte aligned buffers.  Persistent: one CTA per SM.
+bool envelope_tc_supported(int64_t T);
 cudaError_t envelope_tc_configure();
 cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
-                               bool bf16, int sm_count, cudaStream_t st);
+                               int sm_count, cudaStream_t st);
 cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out,
                                     int32_t decim, const float* lp, int32_t L, const float* bp, int32_t Lb,
                                     cudaStream_t st);

@@ -80,7 +80,7 @@ struct dmas_plan_s {
   dmas::LpTaps127 lp127{};
   bool lp_fast = false;               // FP32 FIR fast path (127 taps, R = 1, no band-pass)
   bool lp_tc = false;                 // tensor-core low-pass (L <= 127, R = 1, no band-pass)
-  int32_t env_engine = 0;             // 0 auto (tensor cores, BF16 split), 1 FP32 FIR, 2 tensor cores TF32 split
+  int32_t env_engine = 0;             // 0 auto (tensor cores, BF16 split), 1 FP32 FIR
   int sm_count = 148;
 
   // device state
@@ -204,7 +204,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->bp_taps > 0 && d->lp_taps == 0) return fail(DMAS_ERR_INVALID, "band-pass needs the envelope stage");
   if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
-  if (d->env_engine < 0 || d->env_engine > 2) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1, 2}");
+  if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
   for (int i = 0; i < d->n_mics; ++i)
     if (!finite3(d->mic_xyz + 3 * i)) return fail(DMAS_ERR_INVALID, "non-finite microphone position");
   if (d->reference_xyz && !finite3(d->reference_xyz)) return fail(DMAS_ERR_INVALID, "non-finite reference");
@@ -253,7 +253,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
     const bool aligned16 = ((uintptr_t)y % 16 == 0) && ((uintptr_t)o % 16 == 0);
     if (p->lp_tc && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, st, [&] {
-        return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->env_engine != 2, p->sm_count, st);
+        return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->sm_count, st);
       }));
     } else if (p->lp_fast && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, st, [&] { return dmas::launch_envelope_lp127(y, o, rows, p->T, p->lp127, st); }));
@@ -481,8 +481,8 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     }
     p->lp_fast = (p->lp_taps == dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 && p->T % 4 == 0);
     p->env_engine = desc->env_engine;
-    p->lp_tc = (desc->env_engine != 1 && p->lp_taps <= dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 &&
-                p->T % 4 == 0);
+    p->lp_tc = (desc->env_engine == 0 && p->lp_taps <= dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 &&
+                dmas::envelope_tc_supported(p->T));
     if (p->lp_fast || p->lp_tc)
       for (int i = 0; i < p->lp_taps; ++i) p->lp127.h[i] = p->h_lp[i];
     if (p->lp_tc) PLAN_TRY(dmas::envelope_tc_configure());

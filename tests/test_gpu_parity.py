@@ -342,12 +342,12 @@ def test_timing_and_launch_counter(dm):
     assert all(ms > 0 for ms, c in t.values() if c)
 
 
-@pytest.mark.parametrize("engine", [0, 1, 2])
-@pytest.mark.parametrize("T,L", [(4096, 127), (4132, 127), (8192, 127), (256, 63), (700, 1), (4, 127)])
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("T,L", [(4096, 127), (4160, 127), (4132, 127), (8192, 127), (256, 63), (704, 1), (32, 127)])
 def test_envelope_engines(dm, engine, T, L):
-    """Envelope through the tensor-core low-pass (engine 0: tcgen05 with a 3-pass BF16 split;
-    engine 2: 3-pass TF32 split; 4096-sample tiles, ragged last tile) and the FP32 FIR (engine 1),
-    each against the oracle."""
+    """Envelope through the tensor-core low-pass (engine 0: tcgen05 with a 3-pass BF16 split,
+    4096-sample tiles, ragged last tile, T % 32 == 0; other T fall back to the FP32 FIR) and the
+    FP32 FIR (engine 1), each against the oracle."""
     mic = gen.disk_array(8, 0.05, 5e-3, seed=60)
     dirs = gen.az_el_grid(9, 60.0, 3, 20.0)
     sig = gen.random_signals(2, 8, T, seed=61 + T, sparsity=0.2)
