@@ -24,12 +24,13 @@
 // outside the row are zero-filled by TMA), the store box 128 blocks (blocks past the row end are
 // clipped).  Requires T % 32 == 0 and 16-byte aligned buffers (the plan falls back otherwise).
 //
-// Per CTA (persistent, 1 CTA / SM, warp-specialised, mbarrier pipelines):
+// Per CTA (persistent, 1 CTA / SM, warp-specialised roles linked by mbarriers, every stage
+// double- or quad-buffered so the roles run concurrently):
 //   warp 17 lane 0  TMA producer: 4-slot ring of input tiles
+//   warps 8..15     converters: stage -> |.| -> BF16 hi / lo, once per sample, into a swizzled buffer
+//   warps 0..3      copy: the 5 block-shifted A copies of each TMEM lane (tcgen05.st.x16), hi and lo
 //   warp 16 lane 0  MMA issuer: 30 tcgen05.mma per tile into one of two TMEM accumulators
-//   warps 0..15     converters (stage -> |.| -> BF16 hi/lo once per sample into a swizzled smem
-//                   buffer, then tcgen05.st of the 5 block-shifted A copies of each TMEM lane)
-//                   and epilogue (tcgen05.ld -> clamp -> swizzled smem -> TMA store)
+//   warps 4..7      epilogue: tcgen05.ld.x32 -> clamp -> swizzled smem -> TMA tensor store
 
 #include <cstdint>
 #include <cuda.h>
@@ -49,11 +50,20 @@ constexpr int IN_BLOCKS = TILE_BLOCKS + 2 * HALO;   // 132 rows per input box
 constexpr int ROW_BYTES = BLK * 4;                  // 128 B per block row (fp32)
 constexpr int STAGE_BYTES = 17408;                  // 132 * 128 rounded up to 1024 (swizzle atom)
 constexpr int OUT_BYTES = TILE_BLOCKS * ROW_BYTES;  // 16384
-constexpr int NSTAGE = 4;
+#ifndef DMAS_TC_NSTAGE
+#define DMAS_TC_NSTAGE 6
+#endif
+constexpr int NSTAGE = DMAS_TC_NSTAGE;
 constexpr int NOUT = 2;
-constexpr int CONV_WARPS = 16;
+// warp roles
+constexpr int COPY_WARP0 = 0;                       // warps 0..3: shifted A copies -> TMEM (lane quarter = warp)
+constexpr int EPI_WARP0 = 4;                        // warps 4..7: TMEM accumulator -> clamp -> TMA store
+constexpr int CONV_WARP0 = 8;                       // warps 8..15: fp32 stage -> bf16 hi / lo buffer
+constexpr int CONV_WARPS = 8;
+constexpr int MMA_WARP = 16;
+constexpr int TMA_WARP = 17;
 constexpr int CONV_THREADS = CONV_WARPS * 32;
-constexpr int THREADS = CONV_THREADS + 64;          // + MMA warp + TMA warp
+constexpr int THREADS = 18 * 32;
 
 // H_q^T in shared memory: K-major canonical layout, no swizzle, 8 bf16 per 16-byte core row.
 constexpr int B_LBO = BLK * 16;                     // 512 B between K core columns
@@ -106,6 +116,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 #endif
 }
+#ifdef DMAS_TC_PROFILE
+__device__ unsigned long long g_tc_prof[148][8];
+#define PROF_WAIT(slot, expr)                          \
+  do {                                                 \
+    const unsigned long long t0_ = clock64();          \
+    expr;                                              \
+    prof[slot] += clock64() - t0_;                     \
+  } while (0)
+#else
+#define PROF_WAIT(slot, expr) expr
+#endif
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
@@ -139,6 +160,28 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b,
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
                "r"(d)
                : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&v)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z), "r"(v[1].w),
+      "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z), "r"(v[3].w)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];
@@ -193,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t stage_full[NSTAGE], stage_empty[NSTAGE];
-  __shared__ __align__(8) uint64_t a_full[2], mma_done[2], d_empty[2];
+  __shared__ __align__(8) uint64_t conv_full[2], conv_empty[2], a_full[2], mma_done[2], d_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -214,9 +257,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       mbar_init(&stage_empty[s], CONV_THREADS);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], CONV_THREADS);
+      mbar_init(&conv_full[b], CONV_THREADS);
+      mbar_init(&conv_empty[b], 128);
+      mbar_init(&a_full[b], 128);
       mbar_init(&mma_done[b], 1);
-      mbar_init(&d_empty[b], CONV_THREADS);
+      mbar_init(&d_empty[b], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -240,31 +285,37 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = tmem_base_sh;
+#ifdef DMAS_TC_PROFILE
+  unsigned long long prof[2] = {0, 0};
+  const unsigned long long t_start = clock64();
+#endif
 
-  if (warp == CONV_WARPS + 1) {
+  if (warp == TMA_WARP) {
     // ================= TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&in_map) : "memory");
       for (int64_t jj = 0; jj < my_tiles; ++jj) {
         const int slot = (int)(jj % NSTAGE);
-        if (jj >= NSTAGE) mbar_wait(&stage_empty[slot], (uint32_t)(((jj - NSTAGE) / NSTAGE) & 1));
+        if (jj >= NSTAGE) PROF_WAIT(0, mbar_wait(&stage_empty[slot], (uint32_t)(((jj - NSTAGE) / NSTAGE) & 1)));
         mbar_expect_tx(&stage_full[slot], IN_BLOCKS * ROW_BYTES);
         tma_load_3d(smem + OFF_STAGE + slot * STAGE_BYTES, &in_map, 0, tile_blk(jj) - HALO, (int)tile_row(jj),
                     &stage_full[slot]);
       }
     }
-  } else if (warp == CONV_WARPS) {
-    // ================= MMA issuer: 5 shifts x 2 K-steps x 3 split products per tile (TS mode)
-    if (lane == 0) {
-      const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
-      for (int64_t jj = 0; jj < my_tiles; ++jj) {
-        const int buf = (int)(jj & 1);
-        mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1));
-        if (jj >= 2) mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * BLK);
-        const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
-        uint32_t acc = 0;
+  } else if (warp == MMA_WARP) {
+    // ================= MMA issuer (whole warp runs the loop so every operand is warp-uniform and
+    // lives in uniform registers; one elected lane issues): 5 shifts x 2 K-steps x 3 passes, TS mode
+    const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
+    for (int64_t jj = 0; jj < my_tiles; ++jj) {
+      const int buf = (int)(jj & 1);
+      PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
+      if (jj >= 2) PROF_WAIT(1, mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * BLK);
+      const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
+      uint32_t is_leader;
+      asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(is_leader));
+      if (is_leader) {
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {             // lo*hi, hi*lo, hi*hi
           const uint32_t a_split = (pass == 0) ? (uint32_t)(NQ * A_COLS) : 0u;
@@ -272,85 +323,108 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
 #pragma unroll
           for (int qi = 0; qi < NQ; ++qi) {
 #pragma unroll
-            for (int s = 0; s < BLK / K_MMA; ++s) {
+            for (int s = 0; s < BLK / K_MMA; ++s)
               mma_ts(d, a0 + a_split + (uint32_t)(qi * A_COLS + s * (K_MMA / 2)),
-                     b0 + b_split + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4), acc);
-              acc = 1;
-            }
+                     b0 + b_split + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4), (pass | qi | s) ? 1u : 0u);
           }
         }
         mma_commit(&mma_done[buf]);
       }
+      __syncwarp();
     }
-  } else {
-    // ================= converters + epilogue (warps 0..15): TMEM lane quarter = warp & 3,
-    // sample group (8 samples / 4 packed columns) = warp >> 2
-    const int quarter = warp & 3, grp = warp >> 2;
-    const int tau = 32 * quarter + lane;                   // block (TMEM lane) this thread serves
-    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
-
-    auto epilogue = [&](int64_t jj) {
-      const int buf = (int)(jj & 1), ob = (int)(jj % NOUT);
-      mbar_wait(&mma_done[buf], (uint32_t)((jj >> 1) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[8];
-      tmem_ld8(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * BLK + 8 * grp), v);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&d_empty[buf]);
-      // the store of tile jj - NOUT must have finished reading this staging buffer
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
-      named_bar(1, CONV_THREADS);
-      uint8_t* ost = smem + OFF_OUT + ob * OUT_BYTES;
-      const uint32_t osa = smem_u32(ost);
-      sts128(osa + swz(tau, 2 * grp), make_float4(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f), fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)));
-      sts128(osa + swz(tau, 2 * grp + 1),
-             make_float4(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f), fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, CONV_THREADS);
-      if (tid == 0) {
-        tma_store_3d(&out_map, ost, 0, tile_blk(jj), (int)tile_row(jj));
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    };
-
+  } else if (warp >= CONV_WARP0) {
+    // ================= converters: staged fp32 tile -> |.| -> bf16 hi / lo, once per sample;
+    // conv row r = block -2 + r, chunks 0..3 hi, 4..7 lo (128-byte swizzle)
+    const int ct = tid - CONV_WARP0 * 32;
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int slot = (int)(jj % NSTAGE), buf = (int)(jj & 1);
-      mbar_wait(&stage_full[slot], (uint32_t)((jj / NSTAGE) & 1));
-      if (jj >= 2) mbar_wait(&mma_done[buf], (uint32_t)(((jj - 2) >> 1) & 1));    // A[buf] no longer read
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // (1) convert the staged tile once: fp32 -> |.| -> bf16 hi / lo, row r = block -2 + r
+      PROF_WAIT(0, mbar_wait(&stage_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
+      if (jj >= 2) PROF_WAIT(1, mbar_wait(&conv_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
       const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
       const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
-      for (int i = tid; i < IN_BLOCKS * 8; i += CONV_THREADS) {      // i = (row, fp32 chunk f)
+      for (int i = ct; i < IN_BLOCKS * 8; i += CONV_THREADS) {       // i = (row, fp32 chunk f)
         const int r = i >> 3, f = i & 7;
         const float4 v = lds128(st + swz(r, f));
         uint32_t h01, l01, h23, l23;
         split2(fabsf(v.x), fabsf(v.y), h01, l01);
         split2(fabsf(v.z), fabsf(v.w), h23, l23);
         const uint32_t half = (uint32_t)(f & 1) * 8;
-        sts64(cv + swz(r, f >> 1) + half, h01, h23);                  // hi: chunks 0..3
-        sts64(cv + swz(r, 4 + (f >> 1)) + half, l01, l23);            // lo: chunks 4..7
+        sts64(cv + swz(r, f >> 1) + half, h01, h23);
+        sts64(cv + swz(r, 4 + (f >> 1)) + half, l01, l23);
       }
       mbar_arrive(&stage_empty[slot]);
-      named_bar(2, CONV_THREADS);
-      // (2) the 5 block-shifted copies of this thread's TMEM lane (block tau), hi and lo
-      const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS + 4 * grp);
+      mbar_arrive(&conv_full[buf]);
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ================= epilogue: TMEM accumulator -> clamp -> swizzled smem -> TMA store
+    const int quarter = warp - EPI_WARP0;
+    const int tau = 32 * quarter + lane;
+    const int et = tid - EPI_WARP0 * 32;
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    for (int64_t jj = 0; jj < my_tiles; ++jj) {
+      const int buf = (int)(jj & 1), ob = (int)(jj % NOUT);
+      PROF_WAIT(0, mbar_wait(&mma_done[buf], (uint32_t)((jj >> 1) & 1)));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float v[32];
+      tmem_ld32(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * BLK), v);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&d_empty[buf]);
+      if (et == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
+      named_bar(1, 128);
+      const uint32_t osa = smem_u32(smem + OFF_OUT + ob * OUT_BYTES);
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        sts128(osa + swz(tau, cc), make_float4(fmaxf(v[4 * cc], 0.f), fmaxf(v[4 * cc + 1], 0.f),
+                                               fmaxf(v[4 * cc + 2], 0.f), fmaxf(v[4 * cc + 3], 0.f)));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar(1, 128);
+      if (et == 0) {
+        tma_store_3d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)tile_row(jj));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else {
+    // ================= copy warps: the 5 block-shifted copies of TMEM lane tau (hi and lo)
+    const int quarter = warp - COPY_WARP0;
+    const int tau = 32 * quarter + lane;
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    for (int64_t jj = 0; jj < my_tiles; ++jj) {
+      const int buf = (int)(jj & 1);
+      PROF_WAIT(0, mbar_wait(&conv_full[buf], (uint32_t)((jj >> 1) & 1)));
+      if (jj >= 2) PROF_WAIT(1, mbar_wait(&mma_done[buf], (uint32_t)(((jj - 2) >> 1) & 1)));    // A[buf] free
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
+      const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS);
 #pragma unroll
       for (int qi = 0; qi < NQ; ++qi) {
         const int r = tau + qi;                            // conv row of block tau + q (row 0 = block -2)
-        const uint4 hv = lds128u(cv + swz(r, grp));
-        const uint4 lv = lds128u(cv + swz(r, 4 + grp));
-        tmem_st4(a_col + (uint32_t)(qi * A_COLS), hv.x, hv.y, hv.z, hv.w);
-        tmem_st4(a_col + (uint32_t)(NQ * A_COLS + qi * A_COLS), lv.x, lv.y, lv.z, lv.w);
+        uint4 hv[4], lv[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          hv[g] = lds128u(cv + swz(r, g));
+          lv[g] = lds128u(cv + swz(r, 4 + g));
+        }
+        tmem_st16(a_col + (uint32_t)(qi * A_COLS), hv);
+        tmem_st16(a_col + (uint32_t)(NQ * A_COLS + qi * A_COLS), lv);
       }
+      mbar_arrive(&conv_empty[buf]);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&a_full[buf]);
-      if (jj > 0) epilogue(jj - 1);
     }
-    if (my_tiles > 0) epilogue(my_tiles - 1);
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+#ifdef DMAS_TC_PROFILE
+  if (lane == 0 && blockIdx.x < 148) {
+    const int role = warp == TMA_WARP ? 0 : warp == MMA_WARP ? 1 : warp == CONV_WARP0 ? 2 : warp == EPI_WARP0 ? 3
+                   : warp == COPY_WARP0 ? 4 : -1;
+    if (role == 1) g_tc_prof[blockIdx.x][7] = clock64() - t_start;
+    if (role >= 0) { g_tc_prof[blockIdx.x][role] = prof[0]; if (role >= 1) g_tc_prof[blockIdx.x][role + 1 > 6 ? 6 : role + 1] += 0; }
+    if (role == 1) g_tc_prof[blockIdx.x][5] = prof[1];   // mma: d_empty wait
+    if (role == 2) g_tc_prof[blockIdx.x][6] = prof[1];   // conv: conv_empty wait
+    (void)my_tiles;
+  }
+#endif
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0)
@@ -389,6 +463,12 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t nb
 }  // namespace tc
 
 bool envelope_tc_supported(int64_t T) { return T % tc::BLK == 0 && tc::encode_fn() != nullptr; }
+
+#ifdef DMAS_TC_PROFILE
+extern "C" int dmas_tc_prof_read(unsigned long long* out) {   // debug builds only
+  return cudaMemcpyFromSymbol(out, tc::g_tc_prof, sizeof(tc::g_tc_prof)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 cudaError_t envelope_tc_configure() {
   return cudaFuncSetAttribute(tc::k_envelope_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
