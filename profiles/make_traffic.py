@@ -1,0 +1,38 @@
+"""Write profiles/traffic.json (DRAM bytes per launch per kernel) from `ncu --set full` reports.
+
+usage: python profiles/make_traffic.py <frames_per_launch> <report.ncu-rep> [...]
+Each report holds one captured launch; bytes = dram__bytes_read.sum + dram__bytes_write.sum."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def read(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u, v = rows[0], rows[1], rows[2]
+    get = lambda k: float(v[h.index(k)]) * UNITS[u[h.index(k)]]
+    name = v[h.index("Kernel Name")]
+    return name, get("dram__bytes_read.sum"), get("dram__bytes_write.sum"), float(v[h.index("gpu__time_duration.sum")])
+
+
+def main():
+    frames = int(sys.argv[1])
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    for rep in sys.argv[2:]:
+        name, rd, wr, dur = read(rep)
+        key = "k_beamform" if "beamform" in name else "k_envelope" if "envelope" in name else name
+        data[key] = {"kernel": name, "frames_per_launch": frames, "dram_read_bytes": rd, "dram_write_bytes": wr,
+                     "dram_bytes_per_launch": rd + wr, "ncu_duration_ms": dur, "report": os.path.basename(rep)}
+    json.dump(data, open(path, "w"), indent=1)
+    print(json.dumps(data, indent=1))
+
+
+if __name__ == "__main__":
+    main()
