@@ -76,50 +76,63 @@ def _oracle_chunk(job):
     return e.shape[0] * e.shape[1]
 
 
-def oracle_rate(cfg, frame_idx=0, dirs_per_core=0, cores=None):
+def oracle_rate(cfg, frame_idx=0, dirs_per_core=0, cores=None, pool=None):
     """Time the float64 oracle (as it stands) on a bounded sample of the C5 step: one frame,
-    `cores` x `dirs_per_core` directions, all T samples, CF-DMAS + envelope, one process per
-    core over contiguous direction chunks.  Returns (px/s, cores, sample description)."""
+    `cores` x `dirs_per_core` directions (default: the whole frame), all T samples, CF-DMAS +
+    envelope, one process per core over contiguous direction chunks.  The delay table is built
+    outside the timed region, as in the CUDA path's plan.  Returns (px/s, cores, description)."""
     import multiprocessing as mp
     from oracle import dmas_oracle as O
     cores = cores or os.cpu_count() or 1
-    dpc = dirs_per_core or max(1, len(cfg["dirs"]) // cores)    # default: one whole frame
+    dpc = dirs_per_core or max(1, -(-len(cfg["dirs"]) // cores))    # default: one whole frame
     n = min(len(cfg["dirs"]), cores * dpc)
     sel = np.linspace(0, len(cfg["dirs"]) - 1, n).astype(int)
     d = O.delay_table(cfg["mic_xyz"], cfg["dirs"][sel], cfg["fs"], cfg["c"])
     jobs = [(cfg["signals"][frame_idx], d[i:i + dpc], cfg["order"]) for i in range(0, n, dpc)]
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    try:
+        t0 = time.perf_counter()
         px = sum(pool.map(_oracle_chunk, jobs))
-    dt = time.perf_counter() - t0
-    desc = (f"frame {frame_idx} of C5, {n} of {len(cfg['dirs'])} directions (evenly spaced) x {cfg['T']} samples "
+        dt = time.perf_counter() - t0
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    desc = (f"frame {frame_idx} of C5, {n} of {len(cfg['dirs'])} directions x {cfg['T']} samples "
             f"= {px} px, CF-DMAS p={cfg['order']} + {LP_TAPS}-tap envelope, float64 numpy oracle, "
             f"{cores} processes; {dt:.1f} s")
     return px / dt, cores, desc
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the oracle, as it stands, on the host cores (rank 0 only).  Each step
+    beamforms one whole C5 frame (a bounded sample of the 256-frame step) with a process pool
+    over all cores; value = median px/s over the timed steps."""
+    import multiprocessing as mp
     if rank != 0:
         return 0
     cfg = gen.config(WORKLOAD, frames=1)
     cores = os.cpu_count() or 1
-    times, rates, desc = [], [], ""
-    for i in range(args.warmup + args.steps):
-        r, c, desc = oracle_rate(cfg, 0, args.cpu_dirs or 32, cores)
-        if i >= args.warmup:
-            rates.append(r)
+    rates, desc = [], ""
+    with mp.get_context("fork").Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            r, c, desc = oracle_rate(cfg, 0, args.cpu_dirs, cores, pool)
+            if i >= args.warmup:
+                rates.append(r)
     value = statistics.median(rates)
-    px_step = cfg["n_frames"] * len(cfg["dirs"]) * cfg["T"] * args.frames
+    px_step = len(cfg["dirs"]) * cfg["T"] * args.frames
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * px_step / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "each step times a bounded sample of the C5 step on the host cores; ms_per_step is extrapolated "
-                "linearly (cost is exactly proportional to frames x directions x samples)",
+        "note": "each step times one whole C5 frame (a bounded sample of the 256-frame step) on the host cores; "
+                "ms_per_step is that rate extrapolated linearly to the 256-frame step (cost is exactly "
+                "proportional to frames x directions x samples)",
     }
     print(json.dumps(line), flush=True)
     return 0
