@@ -96,6 +96,9 @@ struct dmas_plan_s {
   size_t scratch_cap = 0;
   // envelope of chunk c runs on env_stream while chunk c+1 beamforms on the caller's stream
   // (k_beamform is FP32-ALU bound, the envelope HBM / tensor-core bound: they overlap)
+  // Off by default: measured on B200 the persistent tensor-core envelope CTA (one per SM, ~55k
+  // registers) cannot co-reside with beamform CTAs, so the kernels only time-share SMs (no gain).
+  bool overlap_env = false;
   cudaStream_t env_stream = nullptr;
   cudaEvent_t ev_bf[2] = {nullptr, nullptr}, ev_env[2] = {nullptr, nullptr};
   bool env_used[2] = {false, false};  // ev_env[b] has been recorded (a previous call may still run)
@@ -259,9 +262,11 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.cf_eps = p->cf_eps;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
-  CUDA_TRY(cudaEventRecord(p->ev_bf[pp], st));
-  cudaStream_t es = p->env_stream;
-  CUDA_TRY(cudaStreamWaitEvent(es, p->ev_bf[pp], 0));
+  cudaStream_t es = p->overlap_env ? p->env_stream : st;
+  if (p->overlap_env) {
+    CUDA_TRY(cudaEventRecord(p->ev_bf[pp], st));
+    CUDA_TRY(cudaStreamWaitEvent(es, p->ev_bf[pp], 0));
+  }
   const int64_t rows = (int64_t)nf * p->n_dirs;
   for (int k = 0; k < dmas::N_KINDS; ++k) {
     if (!((env_kinds >> k) & 1u)) continue;
@@ -281,8 +286,10 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
       }));
     }
   }
-  CUDA_TRY(cudaEventRecord(p->ev_env[pp], es));
-  p->env_used[pp] = true;
+  if (p->overlap_env) {
+    CUDA_TRY(cudaEventRecord(p->ev_env[pp], es));
+    p->env_used[pp] = true;
+  }
   return DMAS_OK;
 }
 
@@ -315,7 +322,8 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
   const int n_scratch = popcount5(env_only);
   const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
   int32_t chunk = std::min(p->chunk_cap, n_frames);
-  if (env_k) {
+  const int halves = p->overlap_env ? 2 : 1;
+  if (env_k && p->overlap_env) {
     if (!p->env_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->env_stream, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
       if (!p->ev_bf[b]) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_bf[b], cudaEventDisableTiming));
@@ -323,9 +331,9 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     }
   }
   if (n_scratch > 0) {
-    const int64_t fit = p->scratch_budget / (int64_t)(2 * frame_img * n_scratch);   // two ping-pong halves
+    const int64_t fit = p->scratch_budget / (int64_t)(halves * frame_img * n_scratch);   // ping-pong halves
     chunk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(chunk, fit));
-    const size_t need = 2 * (size_t)chunk * n_scratch * frame_img;
+    const size_t need = halves * (size_t)chunk * n_scratch * frame_img;
     if (need > p->scratch_cap) {
       CUDA_TRY(cudaStreamSynchronize(st));
       if (p->env_stream) CUDA_TRY(cudaStreamSynchronize(p->env_stream));
@@ -338,11 +346,11 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
   }
   // scratch halves may still be read by envelopes of a previous call on another stream
   for (int b = 0; b < 2; ++b)
-    if (env_k && p->env_used[b]) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[b], 0));
+    if (p->env_used[b]) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[b], 0));
   int c = 0;
   for (int32_t f0 = 0; f0 < n_frames; f0 += chunk, ++c) {
     const int32_t nf = std::min(chunk, n_frames - f0);
-    const int pp = c & 1;
+    const int pp = p->overlap_env ? (c & 1) : 0;
     float* scratch_half = p->d_scratch ? p->d_scratch + (size_t)pp * chunk * n_scratch * p->n_dirs * p->T : nullptr;
     float* raw_dst[dmas::N_KINDS] = {};
     float* env_dst[dmas::N_KINDS] = {};
@@ -353,10 +361,10 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
       if ((env_k >> k) & 1u) env_dst[k] = env_user[k] + (size_t)f0 * p->n_dirs * p->T_out;
     }
     const float* sig = signals + (size_t)f0 * p->n_mics * p->T;
-    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, pp, env_k != 0 && c >= 2);
+    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, pp, p->overlap_env && env_k && c >= 2);
     if (rc != DMAS_OK) return rc;
   }
-  if (env_k) {                                   // the caller's stream sees every envelope
+  if (env_k && p->overlap_env) {                 // the caller's stream sees every envelope
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[(c - 1) & 1], 0));
     if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[c & 1], 0));
   }

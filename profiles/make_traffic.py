@@ -9,7 +9,8 @@ import os
 import subprocess
 import sys
 
-UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}  # -> ms
 
 
 def read(rep):
@@ -18,7 +19,7 @@ def read(rep):
     h, u, v = rows[0], rows[1], rows[2]
     get = lambda k: float(v[h.index(k)]) * UNITS[u[h.index(k)]]
     name = v[h.index("Kernel Name")]
-    return name, get("dram__bytes_read.sum"), get("dram__bytes_write.sum"), float(v[h.index("gpu__time_duration.sum")])
+    return name, get("dram__bytes_read.sum"), get("dram__bytes_write.sum"), get("gpu__time_duration.sum")
 
 
 def main():
