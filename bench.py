@@ -38,7 +38,6 @@ from workloads import gen  # noqa: E402
 
 METRIC = "CF-DMAS images/sec (directions x range samples per second) at 1/2/4/8 B200"
 UNIT = "px/s"
-WORKLOAD = "C5"
 LP_TAPS = 127
 FP32_LANES_PER_SM_CLK = 128     # FFMA/FADD/FMUL lanes per SM per clock (B200, measured 124-128)
 
@@ -49,7 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--frames", type=int, default=256, help="frames per step (C5: 256)")
+    ap.add_argument("--frames", type=int, default=0, help="frames per step (0: the workload's, C5 256, C4 16)")
+    ap.add_argument("--workload", choices=["C5", "C4"], default="C5",
+                    help="C5 = the metric's config (default); C4 = 64-mic p = 3 secondary line")
     ap.add_argument("--mode", choices=["weak", "dirshard"], default="weak")
     ap.add_argument("--e2e-frames", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -100,7 +101,7 @@ def oracle_rate(cfg, frame_idx=0, dirs_per_core=0, cores=None, pool=None):
         if own:
             pool.close()
             pool.join()
-    desc = (f"frame {frame_idx} of C5, {n} of {len(cfg['dirs'])} directions x {cfg['T']} samples "
+    desc = (f"frame {frame_idx} of {cfg['name']}, {n} of {len(cfg['dirs'])} directions x {cfg['T']} samples "
             f"= {px} px, CF-DMAS p={cfg['order']} + {LP_TAPS}-tap envelope, float64 numpy oracle, "
             f"{cores} processes; {dt:.1f} s")
     return px / dt, cores, desc
@@ -113,7 +114,7 @@ def run_reference(args, rank, world):
     import multiprocessing as mp
     if rank != 0:
         return 0
-    cfg = gen.config(WORKLOAD, frames=1)
+    cfg = gen.config(args.workload, frames=1)
     cores = os.cpu_count() or 1
     rates, desc = [], ""
     with mp.get_context("fork").Pool(cores) as pool:
@@ -149,12 +150,27 @@ def load_traffic():
         return {}
 
 
+WORKLOADS = {
+    "C5": {"array": "32-mic eRTIS-like disk (10 cm)", "n_dirs": 16384, "grid": "128 az (+-90) x 128 el (+-60)",
+           "n_samples": 4096, "fs_hz": 450000, "order": 2, "frames": 256,
+           "l2": "inputs 128 MiB/GPU > 126 MB L2 and every step streams 64 GiB of output (no L2 reuse across steps)"},
+    "C4": {"array": "64-mic disk (10 cm)", "n_dirs": 16384, "grid": "128 az (+-90) x 128 el (+-60)",
+           "n_samples": 8192, "fs_hz": 450000, "order": 3, "frames": 16,
+           "l2": "every step streams 8 GiB of output (no L2 reuse across steps)"},
+}
+# FP32-pipe lane-ops per microphone sample of k_beamform (acc_add<P>) and per pixel
+# epilogue (Newton-Girard + CF + CF product)
+OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
+OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
+
+
 def config_dict(args, world):
-    return {"workload": WORKLOAD, "array": "32-mic eRTIS-like disk (10 cm)", "n_dirs": 16384,
-            "grid": "128 az (+-90) x 128 el (+-60)", "n_samples": 4096, "fs_hz": 450000, "order": 2,
-            "frames_per_step_per_gpu": args.frames, "outputs": "CF-DMAS envelope (127-tap 5 kHz low-pass)",
-            "mode": args.mode, "world": world,
-            "l2": "inputs 128 MiB/GPU > 126 MB L2 and every step streams 64 GiB of output (no L2 reuse across steps)"}
+    w = WORKLOADS[args.workload]
+    return {"workload": args.workload, "array": w["array"], "n_dirs": w["n_dirs"], "grid": w["grid"],
+            "n_samples": w["n_samples"], "fs_hz": w["fs_hz"], "order": w["order"],
+            "frames_per_step_per_gpu": args.frames,
+            "outputs": f"CF-DMAS{w['order']} envelope (127-tap 5 kHz low-pass)",
+            "mode": args.mode, "world": world, "l2": w["l2"]}
 
 
 # ------------------------------------------------------------------ clocks
@@ -208,7 +224,7 @@ def physical_gpu_index(local: int) -> int:
 def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_cfg = gen.config(WORKLOAD, frames=1)
+        cpu_cfg = gen.config(args.workload, frames=1)
         r, c, desc = oracle_rate(cpu_cfg, 0, args.cpu_dirs, None)
         cpu = {"value": r, "unit": UNIT, "cores": c, "kind": "oracle", "sample": desc}
 
@@ -223,11 +239,12 @@ def run_ours(args, rank, world, local):
 
     # ---- inputs (resident in HBM before the timed region)
     if args.mode == "weak":
-        cfg = gen.config(WORKLOAD, frames=args.frames, stream=rank)
+        cfg = gen.config(args.workload, frames=args.frames, stream=rank)
         dirs = cfg["dirs"]
         x = torch.from_numpy(cfg["signals"]).to(dev)
     else:
-        cfg = gen.config(WORKLOAD, frames=args.frames, stream=0) if rank == 0 else gen.config(WORKLOAD, frames=1)
+        cfg = (gen.config(args.workload, frames=args.frames, stream=0) if rank == 0
+               else gen.config(args.workload, frames=1))
         g0, g1 = parallel.partition(len(cfg["dirs"]), world, rank)
         dirs = cfg["dirs"][g0:g1]
         x = torch.empty((args.frames, cfg["mic_xyz"].shape[0], cfg["T"]), dtype=torch.float32, device=dev)
@@ -282,7 +299,7 @@ def run_ours(args, rank, world, local):
     rt_ms, rt_n = ktime["signed_roots"]
     px_launch_bf = (F * len(dirs) * T) / max(1, bf_n / args.steps)   # pixels per beamform launch
     n_mics = cfg["mic_xyz"].shape[0]
-    ops_bf = 5 * n_mics + 6                      # FP32 pipe lane-ops per pixel
+    ops_bf = OPS_PER_MIC[p] * n_mics + OPS_EPI[p]   # FP32 pipe lane-ops per pixel
     ops_env = LP_TAPS                            # one FFMA per tap per pixel
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
@@ -370,6 +387,8 @@ def run_ours(args, rank, world, local):
 
 def main():
     args = parse()
+    if args.frames <= 0:
+        args.frames = WORKLOADS[args.workload]["frames"]
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)

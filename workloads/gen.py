@@ -151,9 +151,12 @@ def config(name: str, frames=None, stream: int = 0):
     elif name == "C4":
         mic = disk_array(64, 0.10, 4e-3, seed=11)
         dirs = az_el_grid(128, 90.0, 128, 60.0)
-        T, p, F = 8192, 3, 1
-        refl = random_reflectors(3, dirs, 0.5, 2.9, 0.3, 1.0, seed=4)
-        sig = frame(mic, refl, T, snr_db=10.0, seed=4)[None]
+        T, p = 8192, 3
+        F = 1 if frames is None else int(frames)
+        refl = random_reflectors(3, dirs, 0.5, 2.9, 0.3, 1.0, seed=4 + 7919 * stream)
+        sig = np.empty((F, mic.shape[0], T), dtype=np.float32)
+        for f in range(F):                          # frame 0 is the parity frame (noise seed 4)
+            sig[f] = frame(mic, refl, T, snr_db=10.0, seed=4 + f + 1_000_003 * stream)
     elif name == "C5":
         mic = disk_array(32, 0.10, 6e-3, seed=7)
         dirs = az_el_grid(128, 90.0, 128, 60.0)
