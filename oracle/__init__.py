@@ -30,6 +30,7 @@ from .dmas_oracle import (  # noqa: F401
     esp_vieta,
     gather,
     lpf_taps,
+    matched_filter,
     newton_girard_explicit,
     newton_girard_general,
     power_sums,

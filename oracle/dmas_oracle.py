@@ -23,7 +23,7 @@ from fractions import Fraction
 
 import numpy as np
 
-# Output image kinds, in the bit order of the C ABI's output mask (DESIGN.md §Boundary).
+# Output image kinds, in the bit order of the C ABI's output mask (DESIGN.md §1).
 KIND_NAMES = ("das", "dmas", "cfdmas", "cfdas", "cf")
 
 
@@ -78,6 +78,25 @@ def delay_table(mic_xyz, dir_az_el, fs: float, c: float, reference=None, return_
             if return_exact:
                 v_exact[a, i] = v
     return (d, v_exact) if return_exact else d
+
+
+# --------------------------------------------------------------------------------------
+# A0  Matched filter (pulse compression)   (step 1 of the pipeline; NEXT-1)
+# --------------------------------------------------------------------------------------
+def matched_filter(raw, w, T: int):
+    """m_i(t) = sum_k w[k] raw_i[t + k] / sum_k w[k]^2  for t in [0, T)   ("convolved
+    with the known emitted source signal" = correlation with the emitted chirp w; reading Q19:
+    normalised by the chirp energy so an exact unit echo peaks at 1, output sample t = echo onset
+    t, input length T + L - 1).  Direct form, float64.  ``raw``: [..., >= T + L - 1]."""
+    raw = np.asarray(raw, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    L = w.shape[0]
+    if raw.shape[-1] < T + L - 1:
+        raise ValueError("raw recording shorter than T + L - 1")
+    out = np.zeros(raw.shape[:-1] + (T,), dtype=np.float64)
+    for k in range(L):
+        out += w[k] * raw[..., k:k + T]
+    return out / np.sum(w * w)
 
 
 # --------------------------------------------------------------------------------------

@@ -362,3 +362,40 @@ def test_pipeline_peak_and_dynamic_range_trend():
         assert dr > prev
         assert dyn_range(img["cfdmas"]) > dr
         prev = dr
+
+
+# ----------------------------------------------------------------- A0 matched filter (NEXT-1)
+def test_matched_filter_worked_examples():
+    """the emitted signal itself peaks at 1 at lag 0; a copy delayed by 100
+    samples peaks at sample 100 (>= 0.999); zeros stay zeros."""
+    w = gen.chirp_samples()
+    L = len(w)
+    y = O.matched_filter(np.concatenate([w, np.zeros(L)]), w, 1)
+    assert y[0] == pytest.approx(1.0, rel=1e-12)
+    raw = np.zeros(400 + 2 * L)
+    raw[100:100 + L] = w
+    y = O.matched_filter(raw, w, 400)
+    assert int(np.argmax(y)) == 100 and y[100] >= 0.999
+    assert np.all(O.matched_filter(np.zeros((2, 50 + L)), w, 51) == 0)
+
+
+def test_matched_filter_definition_and_library_cases():
+    """Brute force on a tiny case, numpy.correlate ('valid'), linearity, and the generator's
+    independent FFT implementation."""
+    rng = np.random.default_rng(70)
+    w = rng.standard_normal(7)
+    raw = rng.standard_normal((3, 40))
+    T = 40 - 7 + 1
+    y = O.matched_filter(raw, w, T)
+    E = float(np.sum(w * w))
+    for c in range(3):
+        brute = [sum(w[k] * raw[c, t + k] for k in range(7)) / E for t in range(T)]
+        np.testing.assert_allclose(y[c], brute, rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(y[c], np.correlate(raw[c], w, "valid") / E, rtol=1e-12, atol=1e-13)
+    raw2 = rng.standard_normal((3, 40))
+    np.testing.assert_allclose(O.matched_filter(2 * raw - 3 * raw2, w, T), 2 * y - 3 * O.matched_filter(raw2, w, T),
+                               rtol=1e-12, atol=1e-12)
+    mic = gen.disk_array(8, 0.05, 5e-3, seed=2)
+    r = gen.raw_frame(mic, [(0.3, 0.1, 0.6, 1.0)], 800, snr_db=0.0, seed=1)
+    np.testing.assert_allclose(O.matched_filter(r, gen.chirp_samples(), 800), gen.matched_filter(r, 800),
+                               rtol=1e-9, atol=1e-9)

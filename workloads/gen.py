@@ -102,14 +102,20 @@ def matched_filter(raw, T: int, fs: float = FS):
     return y / np.sum(w * w)
 
 
-def frame(mic_xyz, reflectors, T: int, snr_db=None, seed: int = 0, fs: float = FS, c: float = C_SOUND):
-    """One matched-filtered fp32 frame [n_mics][T]."""
+def raw_frame(mic_xyz, reflectors, T: int, snr_db=None, seed: int = 0, fs: float = FS, c: float = C_SOUND):
+    """One raw (not matched-filtered) recording [n_mics][T + L], float64: echoes + noise."""
     L = int(round(CHIRP_DUR * fs))
     raw = echoes(mic_xyz, reflectors, T + L, fs, c)
     if snr_db is not None:
         eta = 10.0 ** (-snr_db / 20.0)
         rng = np.random.Generator(np.random.PCG64(seed))
         raw = raw + eta * rng.standard_normal(raw.shape)
+    return raw
+
+
+def frame(mic_xyz, reflectors, T: int, snr_db=None, seed: int = 0, fs: float = FS, c: float = C_SOUND):
+    """One matched-filtered fp32 frame [n_mics][T]."""
+    raw = raw_frame(mic_xyz, reflectors, T, snr_db, seed, fs, c)
     y = matched_filter(raw, T, fs).astype(np.float32)
     y[np.abs(y) < 1e-30] = 0.0                     # no denormal-vs-FTZ ambiguity
     return y
@@ -171,6 +177,25 @@ def config(name: str, frames=None, stream: int = 0):
         raise KeyError(name)
     return dict(name=name, mic_xyz=mic, dirs=dirs, fs=FS, c=C_SOUND, order=p, T=T,
                 signals=np.ascontiguousarray(sig), n_frames=sig.shape[0])
+
+
+def raw_config(name: str, frames=None):
+    """Raw-recording variant of a config for the matched-filter path (NEXT-1): same scene, signals
+    are the fp32 raw recordings [F][n_mics][T + L - 1] before pulse compression, plus the emitted
+    chirp `chirp` [L] (the matched-filter template)."""
+    cfg = config(name, frames=1)                 # geometry / grid / order only
+    F = 1 if frames is None else int(frames)
+    L = int(round(CHIRP_DUR * FS))
+    mic, T = cfg["mic_xyz"], cfg["T"]
+    scenes = {"C1": ([(math.radians(20.0), 0.0, 600 / FS * C_SOUND / 2, 1.0)], None),
+              "C2": ([(math.radians(10.0), math.radians(5.0), 1.0, 1.0)], None),
+              "C3": (random_reflectors(5, cfg["dirs"], 0.3, 1.45, 0.2, 1.0, seed=3), 0.0)}
+    refl, snr = scenes.get(name, (random_reflectors(3, cfg["dirs"], 0.3, 1.0, 0.3, 1.0, seed=5), 10.0))
+    sig = np.empty((F, mic.shape[0], T + L - 1), dtype=np.float32)
+    for f in range(F):
+        sig[f] = raw_frame(mic, refl, T, snr_db=snr, seed=3 + f)[:, :T + L - 1].astype(np.float32)
+    cfg.update(signals=np.ascontiguousarray(sig), n_frames=F, chirp=chirp_samples(FS).astype(np.float32))
+    return cfg
 
 
 def random_signals(F: int, n_mics: int, T: int, seed: int, scale: float = 1.0, sparsity: float = 0.0):
