@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--workload", choices=["C5", "C4"], default="C5",
                     help="C5 = the metric's config (default); C4 = 64-mic p = 3 secondary line")
     ap.add_argument("--mode", choices=["weak", "dirshard"], default="weak")
+    ap.add_argument("--raw", action="store_true",
+                    help="raw recordings in: the step includes the GPU matched filter (paper Fig. 1 pipeline)")
     ap.add_argument("--e2e-frames", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -170,7 +172,9 @@ def config_dict(args, world):
             "n_samples": w["n_samples"], "fs_hz": w["fs_hz"], "order": w["order"],
             "frames_per_step_per_gpu": args.frames,
             "outputs": f"CF-DMAS{w['order']} envelope (127-tap 5 kHz low-pass)",
-            "mode": args.mode, "world": world, "l2": w["l2"]}
+            "mode": args.mode, "world": world, "l2": w["l2"],
+            "input": "raw recordings, matched filter on the GPU (1125-tap chirp)" if args.raw
+                     else "matched-filtered signals (north_star input)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -238,7 +242,11 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs (resident in HBM before the timed region)
-    if args.mode == "weak":
+    if args.raw:
+        cfg = gen.raw_config(args.workload, frames=args.frames)
+        dirs = cfg["dirs"]
+        x = torch.from_numpy(cfg["signals"]).to(dev)
+    elif args.mode == "weak":
         cfg = gen.config(args.workload, frames=args.frames, stream=rank)
         dirs = cfg["dirs"]
         x = torch.from_numpy(cfg["signals"]).to(dev)
@@ -251,7 +259,8 @@ def run_ours(args, rank, world, local):
         if rank == 0:
             x.copy_(torch.from_numpy(cfg["signals"]))
     F, T, p = args.frames, cfg["T"], cfg["order"]
-    plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, max_frames=F, lp_taps=LP_TAPS, device=local)
+    plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, max_frames=F, lp_taps=LP_TAPS, device=local,
+                     mf_coeffs=cfg.get("chirp") if args.raw else None)
     what = dmas.ENV(dmas.KIND_CFDMAS)
     out = torch.empty((F, len(dirs), T), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -346,7 +355,7 @@ def run_ours(args, rank, world, local):
 
     # ---- end to end through the public API with host buffers (pinned), copies in the timed region
     e2e = None
-    if not args.no_e2e and args.mode == "weak":
+    if not args.no_e2e and args.mode == "weak" and not args.raw:
         Fe = min(args.e2e_frames, F)
         hsig = torch.from_numpy(cfg["signals"][:Fe]).pin_memory()
         hout = torch.empty((Fe, len(dirs), T), dtype=torch.float32).pin_memory()

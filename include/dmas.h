@@ -88,6 +88,13 @@ typedef struct {
                                 (error <= ~1.1e-5 of the envelope) when lp_taps <= 127, no
                                 band-pass, R == 1, T % 32 == 0 and 16-byte aligned buffers,
                                 else the FP32 FIR; 1 = always the FP32 FIR                      */
+  /* Optional matched filter (pulse compression; NEXT-1).  When mf_taps > 0 the
+     signals given to dmas_beamform* are RAW recordings of n_samples + mf_taps - 1 samples per
+     channel, and each channel is first correlated with the emitted signal:
+       m_i(t) = sum_k mf_coeffs[k] raw_i(t + k) / sum_k mf_coeffs[k]^2 ,  t in [0, n_samples)
+     (an exact unit echo starting at sample t peaks at 1 at t).  0 = signals are matched-filtered. */
+  int32_t mf_taps;           /* 0 (default) or 1..16384                                         */
+  const float* mf_coeffs;    /* [mf_taps] host, copied (the emitted chirp)                      */
   /* Runtime. */
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an
@@ -107,7 +114,8 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out);
 
 /* Beamform n_frames frames, asynchronously on `cuda_stream` (a cudaStream_t; NULL = legacy
    default stream).  Returns after enqueueing.
-     signals : DEVICE, fp32 [n_frames][n_mics][n_samples], t contiguous, caller-owned, read-only.
+     signals : DEVICE, fp32 [n_frames][n_mics][n_samples] (or [.][.][n_samples + mf_taps - 1] raw
+               samples when the plan has a matched filter), t contiguous, caller-owned, read-only.
      outs    : HOST array of DEVICE pointers, one per requested (stage, kind): first the raw kinds
                of `what` in bit order, then the envelope kinds in bit order.  Raw outputs are fp32
                [n_frames][n_dirs][n_samples]; envelope outputs are fp32

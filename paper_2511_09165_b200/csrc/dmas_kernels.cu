@@ -87,6 +87,75 @@ cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t row
 }
 
 // ------------------------------------------------------------------------------------------
+// K0+K2 — matched filter fused with the signed roots (NEXT-1):
+//   m[t] = (sum_k w[k] raw[t + k]) / sum_k w^2 ,  S[t] = sgn(m) |m|^(1/p),  t in [0, T)
+// CTA = one (frame, mic) row x 1024 outputs; taps (zero-padded to a multiple of 4) and the raw
+// window in shared memory; each thread produces 4 consecutive outputs from two sliding float4
+// registers (conflict-free LDS.128; the tap float4 is a broadcast): 16 FFMA per 2 LDS.128.
+// ------------------------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(MF_THREADS) k_mf_roots(const float* __restrict__ raw, int64_t T_raw,
+                                                         const float* __restrict__ w, int32_t Lp, float inv_energy,
+                                                         float* __restrict__ S, int64_t T, int64_t Tp, int64_t G) {
+  extern __shared__ __align__(16) float msm[];
+  float* tw = msm;                                   // [Lp] taps
+  float* win = msm + Lp;                             // [MF_T + Lp] raw window
+  const int64_t row = blockIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.y * MF_T;
+  const float* rr = raw + row * T_raw;
+  for (int i = threadIdx.x; i < Lp; i += MF_THREADS) tw[i] = __ldg(w + i);
+  for (int i = threadIdx.x; i < MF_T + Lp; i += MF_THREADS) {
+    const int64_t t = t0 + i;
+    win[i] = (t < T_raw) ? __ldg(rr + t) : 0.f;
+  }
+  __syncthreads();
+  const float4* w4 = reinterpret_cast<const float4*>(tw);
+  const float4* r4 = reinterpret_cast<const float4*>(win) + threadIdx.x;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float4 cur = r4[0];
+  for (int c = 0; c < Lp / 4; ++c) {
+    const float4 nxt = r4[c + 1];
+    const float4 wk = w4[c];
+    const float v[8] = {cur.x, cur.y, cur.z, cur.w, nxt.x, nxt.y, nxt.z, nxt.w};
+    const float ww[4] = {wk.x, wk.y, wk.z, wk.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fmaf(ww[r], v[j + r], acc[j]);
+    cur = nxt;
+  }
+  float* sr = S + row * Tp + G;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t t = t0 + 4 * threadIdx.x + j;
+    if (t < T) sr[t] = signed_root<P>(acc[j] * inv_energy);
+  }
+}
+
+cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const float* w, int32_t Lp, float inv_energy,
+                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, cudaStream_t st) {
+  dim3 grid((unsigned)rows, (unsigned)((T + MF_T - 1) / MF_T));
+  const size_t smem = (size_t)(2 * Lp + MF_T) * sizeof(float);
+  switch (order) {
+    case 2: k_mf_roots<2><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 3: k_mf_roots<3><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 4: k_mf_roots<4><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 5: k_mf_roots<5><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t mf_configure(int32_t Lp) {
+  const int smem = (2 * Lp + MF_T) * (int)sizeof(float);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaFuncSetAttribute(k_mf_roots<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+// ------------------------------------------------------------------------------------------
 // K3 — fused gather + power sums + Newton-Girard + CF.
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -34,6 +34,11 @@ constexpr int ENV_FAST_TAPS = 127;
 constexpr int ENV_RPC = 8;              // rows per CTA (double-buffered staging)
 constexpr int ENV_GEN_T = 256;          // generic path: outputs per CTA
 
+// Matched filter + roots (K0+K2): 1024 outputs of one (frame, mic) row per CTA, 4 per thread.
+constexpr int MF_THREADS = 256;
+constexpr int MF_T = 1024;
+constexpr int MF_MAX_TAPS = 16384;
+
 constexpr int N_KINDS = 5;              // DAS, DMAS, CFDMAS, CFDAS, CF (dmas.h bit order)
 
 struct BeamformArgs {
@@ -56,6 +61,12 @@ cudaError_t launch_delay_table(const double* u /*[n_dirs][3]*/, const double* po
 // K2: S[f][i][G + t] = sgn(m) |m|^(1/p) for t in [0, T) (hoisted signed roots, A3).
 cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp,
                                 int64_t G, cudaStream_t st);
+
+// K0+K2: matched filter (correlation with the zero-padded chirp w[Lp], / energy) fused with the
+// signed roots; raw rows [rows][T_raw], T_raw >= T + L - 1 (NEXT-1).
+cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const float* w, int32_t Lp, float inv_energy,
+                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, cudaStream_t st);
+cudaError_t mf_configure(int32_t Lp);
 
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);

@@ -72,6 +72,10 @@ struct dmas_plan_s {
   int device = 0;
   int32_t n_mics = 0, order = 2, lp_taps = 0, bp_taps = 0, env_decim = 1, max_frames = 1;
   int64_t n_dirs = 0, T = 0, T_out = 0;
+  int64_t T_in = 0;                   // input samples per channel: T, or T + mf_taps - 1 (raw)
+  int32_t mf_taps = 0, mf_lp = 0;     // matched filter taps / padded to a multiple of 4
+  float mf_inv_energy = 0.f;
+  float* d_mf = nullptr;
   double fs = 0, c = 0;
   float cf_eps = 1e-30f;
   int32_t dmin = 0, dmax = 0;
@@ -153,6 +157,7 @@ void free_plan_memory(dmas_plan_s* p) {
   cudaFree(p->d_splane);
   cudaFree(p->d_lp);
   cudaFree(p->d_bp);
+  cudaFree(p->d_mf);
   cudaFree(p->d_scratch);
   for (int b = 0; b < 2; ++b) {
     cudaFree(p->d_hsig[b]);
@@ -218,6 +223,16 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
   if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
+  if (d->mf_taps < 0 || d->mf_taps > dmas::MF_MAX_TAPS) return fail(DMAS_ERR_INVALID, "mf_taps not in [0, 16384]");
+  if (d->mf_taps > 0 && !d->mf_coeffs) return fail(DMAS_ERR_NULL, "mf_coeffs is NULL");
+  if (d->mf_taps > 0) {
+    double e = 0.0;
+    for (int k = 0; k < d->mf_taps; ++k) {
+      if (!std::isfinite(d->mf_coeffs[k])) return fail(DMAS_ERR_INVALID, "non-finite mf_coeffs");
+      e += (double)d->mf_coeffs[k] * d->mf_coeffs[k];
+    }
+    if (!(e > 0.0)) return fail(DMAS_ERR_INVALID, "mf_coeffs has zero energy");
+  }
   for (int i = 0; i < d->n_mics; ++i)
     if (!finite3(d->mic_xyz + 3 * i)) return fail(DMAS_ERR_INVALID, "non-finite microphone position");
   if (d->reference_xyz && !finite3(d->reference_xyz)) return fail(DMAS_ERR_INVALID, "non-finite reference");
@@ -244,9 +259,16 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
                           float* const* env_dst, uint32_t env_kinds, cudaStream_t st, int pp, bool wait_env) {
   // the envelope that read this scratch half two chunks ago must be done before we overwrite it
   if (wait_env) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[pp], 0));
-  CUDA_TRY(timed(p, K_ROOTS, st, [&] {
-    return dmas::launch_signed_roots(p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
-  }));
+  if (p->mf_taps > 0) {
+    CUDA_TRY(timed(p, K_ROOTS, st, [&] {
+      return dmas::launch_mf_roots(p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
+                                   (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
+    }));
+  } else {
+    CUDA_TRY(timed(p, K_ROOTS, st, [&] {
+      return dmas::launch_signed_roots(p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
+    }));
+  }
   dmas::BeamformArgs a{};
   a.splane = p->d_splane;
   a.delays = p->d_delays;
@@ -360,7 +382,7 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
       else if ((env_only >> k) & 1u) raw_dst[k] = scratch_half + (size_t)(s++) * chunk * p->n_dirs * p->T;
       if ((env_k >> k) & 1u) env_dst[k] = env_user[k] + (size_t)f0 * p->n_dirs * p->T_out;
     }
-    const float* sig = signals + (size_t)f0 * p->n_mics * p->T;
+    const float* sig = signals + (size_t)f0 * p->n_mics * p->T_in;
     dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, pp, p->overlap_env && env_k && c >= 2);
     if (rc != DMAS_OK) return rc;
   }
@@ -414,6 +436,8 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   p->bp_taps = desc->bp_taps;
   p->env_decim = desc->env_decim;
   p->T_out = (p->T + p->env_decim - 1) / p->env_decim;
+  p->mf_taps = desc->mf_taps;
+  p->T_in = p->T + (p->mf_taps > 0 ? p->mf_taps - 1 : 0);
   p->scratch_budget = desc->scratch_bytes > 0 ? desc->scratch_bytes : ((int64_t)4 << 30);
 
   auto bail = [&](dmas_status s) {
@@ -513,6 +537,21 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   PLAN_TRY(cudaMalloc(&p->d_splane, plane_frame * p->chunk_cap));
   PLAN_TRY(cudaMemset(p->d_splane, 0, plane_frame * p->chunk_cap));
 
+  // ---- matched filter template (zero-padded to a multiple of 4), 1 / energy in float64
+  if (p->mf_taps > 0) {
+    p->mf_lp = (p->mf_taps + 3) / 4 * 4;
+    std::vector<float> w((size_t)p->mf_lp, 0.f);
+    double e = 0.0;
+    for (int k = 0; k < p->mf_taps; ++k) {
+      w[k] = desc->mf_coeffs[k];
+      e += (double)w[k] * w[k];
+    }
+    p->mf_inv_energy = (float)(1.0 / e);
+    PLAN_TRY(cudaMalloc(&p->d_mf, w.size() * sizeof(float)));
+    PLAN_TRY(cudaMemcpy(p->d_mf, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice));
+    PLAN_TRY(dmas::mf_configure(p->mf_lp));
+  }
+
   // ---- envelope taps
   if (p->lp_taps > 0) {
     std::vector<double> h = blackman_lowpass(p->lp_taps, desc->lp_cutoff_hz, p->fs);
@@ -578,7 +617,7 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
   for (int k = 0; k < dmas::N_KINDS; ++k)
     if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs * p->T_out * sizeof(float));
   for (size_t b : out_frame_bytes) out_frame_total += b;
-  const size_t sig_frame = (size_t)p->n_mics * p->T * sizeof(float);
+  const size_t sig_frame = (size_t)p->n_mics * p->T_in * sizeof(float);
   int32_t hc = (int32_t)std::max<size_t>(1, ((size_t)512 << 20) / out_frame_total);
   hc = std::min({hc, p->max_frames, n_frames});
 
@@ -610,7 +649,7 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
     const int b = chunk_idx & 1;
     const int32_t nf = std::min(hc, n_frames - f0);
     if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[0], d2h_done[b], 0));
-    CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T, sig_frame * nf,
+    CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T_in, sig_frame * nf,
                              cudaMemcpyHostToDevice, p->hs[0]));
     CUDA_TRY(cudaEventRecord(h2d_done[b], p->hs[0]));
     CUDA_TRY(cudaStreamWaitEvent(p->hs[1], h2d_done[b], 0));

@@ -59,6 +59,8 @@ class dmas_plan_desc(ctypes.Structure):
         ("bp_coeffs", ctypes.POINTER(ctypes.c_float)),
         ("env_decim", ctypes.c_int32),
         ("env_engine", ctypes.c_int32),
+        ("mf_taps", ctypes.c_int32),
+        ("mf_coeffs", ctypes.POINTER(ctypes.c_float)),
         ("device", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
     ]
@@ -143,7 +145,8 @@ class Plan:
     def __init__(self, mic_xyz, dir_az_el, fs: float, c: float, order: int, n_samples: int, *,
                  max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
-                 device: int = -1, scratch_bytes: int = 0, env_engine: int = 0):
+                 device: int = -1, scratch_bytes: int = 0, env_engine: int = 0,
+                 mf_coeffs: Optional[Sequence[float]] = None):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -167,6 +170,12 @@ class Plan:
             d.bp_coeffs = bp.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         d.env_decim, d.device, d.scratch_bytes = int(env_decim), int(device), int(scratch_bytes)
         d.env_engine = int(env_engine)
+        self.mf_taps = 0
+        if mf_coeffs is not None and len(mf_coeffs) > 0:
+            mf = np.ascontiguousarray(np.asarray(mf_coeffs, dtype=np.float32))
+            self._keep.append(mf)
+            d.mf_taps = self.mf_taps = mf.shape[0]
+            d.mf_coeffs = mf.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         self._keep += [mic, dirs]
         _check(lib.dmas_plan(ctypes.byref(d), ctypes.byref(self._h)))
         info = dmas_plan_info()
@@ -199,8 +208,9 @@ class Plan:
         import torch
         if not (isinstance(signals, torch.Tensor) and signals.is_cuda and signals.dtype == torch.float32):
             raise TypeError("signals must be a CUDA float32 tensor [F][n_mics][T]")
-        if not signals.is_contiguous() or signals.dim() != 3 or signals.shape[1:] != (self.n_mics, self.n_samples):
-            raise ValueError(f"signals must be contiguous [F][{self.n_mics}][{self.n_samples}], got {tuple(signals.shape)}")
+        n_in = self.n_samples + max(0, self.mf_taps - 1)
+        if not signals.is_contiguous() or signals.dim() != 3 or signals.shape[1:] != (self.n_mics, n_in):
+            raise ValueError(f"signals must be contiguous [F][{self.n_mics}][{n_in}], got {tuple(signals.shape)}")
         F = signals.shape[0]
         shapes = self.out_shapes(F, what)
         if outs is None:
@@ -220,8 +230,8 @@ class Plan:
     def beamform_host(self, signals: np.ndarray, what: int, outs: Optional[list] = None) -> Dict:
         if signals.dtype != np.float32 or not signals.flags.c_contiguous:
             raise TypeError("signals must be C-contiguous float32")
-        if signals.ndim != 3 or signals.shape[1:] != (self.n_mics, self.n_samples):
-            raise ValueError("signals must be [F][n_mics][T]")
+        if signals.ndim != 3 or signals.shape[1:] != (self.n_mics, self.n_samples + max(0, self.mf_taps - 1)):
+            raise ValueError("signals must be [F][n_mics][T (+ mf_taps - 1)]")
         F = signals.shape[0]
         shapes = self.out_shapes(F, what)
         if outs is None:

@@ -90,6 +90,9 @@ def test_validation_errors(dm):
     assert _plan_err(dm, dir_az_el=np.array([[4.0, 0.0]])) == 2                             # theta > pi
     assert _plan_err(dm, dir_az_el=np.array([[0.0, 1.6]])) == 2                             # phi > pi/2
     assert _plan_err(dm, bp_coeffs=[1.0, 2.0]) == 2                                         # even bp length
+    assert _plan_err(dm, mf_coeffs=np.zeros(8)) == 2                                        # zero-energy chirp
+    assert _plan_err(dm, mf_coeffs=np.ones(20000)) == 2                                     # too many taps
+    assert _plan_err(dm, mf_coeffs=np.array([1.0, np.inf])) == 2
 
 
 def test_null_handling(dm):

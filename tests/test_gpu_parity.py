@@ -24,10 +24,10 @@ def dm():
     return dmas
 
 
-def run_gpu(dm, mic, dirs, fs, c, p, signals, what, **kw):
+def run_gpu(dm, mic, dirs, fs, c, p, signals, what, n_samples=None, **kw):
     import torch
     F = signals.shape[0]
-    plan = dm.Plan(mic, dirs, fs, c, p, signals.shape[2], max_frames=max(1, F), **kw)
+    plan = dm.Plan(mic, dirs, fs, c, p, n_samples or signals.shape[2], max_frames=max(1, F), **kw)
     x = torch.from_numpy(np.ascontiguousarray(signals)).cuda()
     res = plan.beamform(x, what)
     torch.cuda.synchronize()
@@ -357,3 +357,36 @@ def test_envelope_engines(dm, engine, T, L):
                         lp_taps=L)
     for key in ref:
         assert_parity(g[key], ref[key], f"engine={engine} T={T} L={L} {key}")
+
+
+# ------------------------------------------------------------------ NEXT-1: matched filter on the GPU
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_matched_filter_pipeline(dm, name):
+    """Raw recordings (T + L - 1 samples, L = 1125-sample chirp) -> GPU matched filter fused with the
+    signed roots -> beamform -> envelope, against oracle matched_filter -> beamform_frame -> envelope."""
+    cfg = gen.raw_config(name, frames=2)
+    p = cfg["order"]
+    T = cfg["T"]
+    plan, g = run_gpu(dm, cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, cfg["signals"],
+                      dm.RAW(dm.KIND_DAS | dm.KIND_CFDMAS | dm.KIND_CF) | dm.ENV(dm.KIND_CFDMAS), n_samples=T,
+                      mf_coeffs=cfg["chirp"])
+    mf = O.matched_filter(cfg["signals"], cfg["chirp"], T)
+    ref = oracle_images(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, mf, kinds=("das", "cfdmas", "cf"),
+                        env_kinds=("cfdmas",))
+    for key in ref:
+        assert_parity(g[key], ref[key], f"MF {name} {key}")
+
+
+def test_matched_filter_host_path_and_validation(dm):
+    import torch
+    cfg = gen.raw_config("C1", frames=3)
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=2,
+                   mf_coeffs=cfg["chirp"])
+    what = dm.ENV(dm.KIND_CFDMAS)
+    host = plan.beamform_host(cfg["signals"], what)
+    dev = plan.beamform(torch.from_numpy(cfg["signals"][:2]).cuda(), what)
+    assert np.array_equal(dev[("env", "cfdmas")].cpu().numpy(), host[("env", "cfdmas")][:2])
+    with pytest.raises(ValueError):                                   # matched-filtered length is rejected
+        plan.beamform(torch.zeros((1, 8, cfg["T"]), device="cuda"), what)
+    with pytest.raises(dm.DmasError):
+        dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], mf_coeffs=np.zeros(16))
