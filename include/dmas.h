@@ -44,7 +44,8 @@ typedef enum {
                            duplicate microphone positions, lp_taps even or <0, lp_cutoff not in
                            (0, fs/2), bp_taps even or <0, env_decim<1, cf_eps<0, delay range
                            too large for int32 windows                                            */
-  DMAS_ERR_ORDER = 3,   /* order p not in [2,5], or n_mics < p (the DMAS sum is empty)             */
+  DMAS_ERR_ORDER = 3,   /* order p not in [2,8], n_mics < p (the DMAS sum is empty), or p >= 6
+                           with n_mics < 2p (fp32 Newton-Girard cancellation)     */
   DMAS_ERR_SHAPE = 4,   /* n_frames<0 or > max_frames; output mask asks for nothing / for an
                            envelope on a plan built with lp_taps == 0; misaligned pointer         */
   DMAS_ERR_CUDA = 5,    /* CUDA runtime/launch error (message in dmas_last_error())               */
@@ -74,7 +75,9 @@ typedef struct {
   const double* reference_xyz; /* [3] phase centre; NULL = origin                               */
   double fs_hz;              /* sample rate, > 0                                                */
   double c_mps;              /* speed of sound, > 0                                             */
-  int32_t order;             /* DMAS order p in [2,5]                                           */
+  int32_t order;             /* DMAS order p in [2,8]: 2..5 use the paper's explicit expansions
+                                (PAPER.md:142-160), 6..8 the general partition formula
+                                 with compile-time coefficient tables             */
   int64_t n_samples;         /* T, samples per channel per frame, >= 1                          */
   int32_t max_frames;        /* upper bound on n_frames per call, >= 1                          */
   float cf_eps;              /* CF denominator guard, >= 0; default 1e-30        */

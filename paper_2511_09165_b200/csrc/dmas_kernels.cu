@@ -57,7 +57,9 @@ __device__ __forceinline__ float signed_root(float v) {
   if (P == 2) r = __fsqrt_rn(a);
   else if (P == 3) r = cbrtf(a);
   else if (P == 4) r = __fsqrt_rn(__fsqrt_rn(a));
-  else r = powf(a, 0.2f);
+  else if (P == 8) r = __fsqrt_rn(__fsqrt_rn(__fsqrt_rn(a)));
+  else if (P == 6) r = cbrtf(__fsqrt_rn(a));
+  else r = powf(a, 1.0f / (float)P);
   return copysignf(r, v);
 }
 
@@ -81,6 +83,9 @@ cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t row
     case 3: k_signed_roots<3><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     case 4: k_signed_roots<4><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     case 5: k_signed_roots<5><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 6: k_signed_roots<6><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 7: k_signed_roots<7><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 8: k_signed_roots<8><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -141,6 +146,9 @@ cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const fl
     case 3: k_mf_roots<3><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     case 4: k_mf_roots<4><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     case 5: k_mf_roots<5><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 6: k_mf_roots<6><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 7: k_mf_roots<7><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 8: k_mf_roots<8><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -152,7 +160,10 @@ cudaError_t mf_configure(int32_t Lp) {
   if ((e = cudaFuncSetAttribute(k_mf_roots<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(k_mf_roots<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(k_mf_roots<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  return cudaFuncSetAttribute(k_mf_roots<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if ((e = cudaFuncSetAttribute(k_mf_roots<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaFuncSetAttribute(k_mf_roots<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -188,13 +199,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // Per-pixel accumulators.  P1..P_{p-1} of the signed roots, P_p (= A for odd p, = sum |x| for
 // even p), A = sum x (DAS) and B = sum x^2 (CF).  Packed in float2 pairs for FADD2/FFMA2.
-template <int P> struct Acc;
+template <int P> struct Acc {                           // P >= 6 (NEXT-3): P_1..P_P, A, B
+  float pk[P];                                          // pk[k-1] = P_k (P_P = A for odd P)
+  float a, b;
+};
 template <> struct Acc<2> { float2 pa, pb; };          // pa = (P1, A), pb = (P2, B)
 template <> struct Acc<3> { float2 p12; float a, b; };  // P3 = A
 template <> struct Acc<4> { float2 p12, p34; float a, b; };
 template <> struct Acc<5> { float2 p12, p34; float a, b; };  // P5 = A
 
-template <int P> __device__ __forceinline__ void acc_zero(Acc<P>& c);
+template <int P> __device__ __forceinline__ void acc_zero(Acc<P>& c) {
+#pragma unroll
+  for (int k = 0; k < P; ++k) c.pk[k] = 0.f;
+  c.a = c.b = 0.f;
+}
 template <> __device__ __forceinline__ void acc_zero<2>(Acc<2>& c) { c.pa = c.pb = make_float2(0.f, 0.f); }
 template <> __device__ __forceinline__ void acc_zero<3>(Acc<3>& c) { c.p12 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
 template <> __device__ __forceinline__ void acc_zero<4>(Acc<4>& c) { c.p12 = c.p34 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
@@ -202,7 +220,18 @@ template <> __device__ __forceinline__ void acc_zero<5>(Acc<5>& c) { c.p12 = c.p
 
 // One microphone sample s = s_i(t, psi) of one pixel.  x = sgn(s)|s|^p is rebuilt from s
 // (exact up to rounding since s^p = sgn(x)^p |x| and the p = 2 / 4 cases take |s|).
-template <int P> __device__ __forceinline__ void acc_add(Acc<P>& c, float s);
+template <int P> __device__ __forceinline__ void acc_add(Acc<P>& c, float s) {
+  float pw = s;                                          // s^k
+  c.pk[0] += s;
+#pragma unroll
+  for (int k = 1; k < P; ++k) {
+    pw *= s;
+    c.pk[k] += pw;                                       // k = P - 1: s^P = x (odd P) or |x| (even P)
+  }
+  const float x = (P & 1) ? pw : copysignf(pw, s);
+  c.a += x;
+  c.b = fmaf(x, x, c.b);
+}
 template <> __device__ __forceinline__ void acc_add<2>(Acc<2>& c, float s) {
   const float2 sx = make_float2(s, s * fabsf(s));   // (s, x)
   c.pa = __fadd2_rn(c.pa, sx);                      // P1 += s, A += x
@@ -236,7 +265,59 @@ template <> __device__ __forceinline__ void acc_add<5>(Acc<5>& c, float s) {
 }
 
 // Newton-Girard explicit expansions, exactly as printed.
-template <int P> __device__ __forceinline__ void acc_final(const Acc<P>& c, float& A, float& B, float& E);
+// General Newton-Girard formula (Eq. PAPER.md:136): E_n = sum over partitions (k_1..k_n) of n with
+// sum_i i k_i = n of (-1)^(n - sum k_i) prod_i P_i^{k_i} / (k_i! i^{k_i}); the partition list and
+// coefficients are generated at compile time (SPEC's "cached coefficient list"), so the epilogue
+// is a fixed sequence of products.
+template <int N> struct PartitionTable {
+  int n = 0;
+  int k[32][N] = {};
+  float coef[32] = {};
+  constexpr PartitionTable() {
+    int ks[N + 1] = {};
+    rec(1, N, ks);
+  }
+  constexpr void rec(int i, int rem, int* ks) {
+    if (i > N) {
+      if (rem != 0) return;
+      double c = 1.0;
+      int parts = 0;
+      for (int j = 1; j <= N; ++j) {
+        parts += ks[j];
+        double fact = 1.0, ipow = 1.0;
+        for (int q = 2; q <= ks[j]; ++q) fact *= q;
+        for (int q = 0; q < ks[j]; ++q) ipow *= j;
+        c /= fact * ipow;
+      }
+      if ((N - parts) & 1) c = -c;
+      for (int j = 1; j <= N; ++j) k[n][j - 1] = ks[j];
+      coef[n] = (float)c;
+      ++n;
+      return;
+    }
+    for (int q = 0; q * i <= rem; ++q) {
+      ks[i] = q;
+      rec(i + 1, rem - q * i, ks);
+    }
+    ks[i] = 0;
+  }
+};
+template <int P> __device__ __forceinline__ void acc_final(const Acc<P>& c, float& A, float& B, float& E) {
+  constexpr PartitionTable<P> tab{};
+  A = c.a;
+  B = c.b;
+  float e = 0.f;
+#pragma unroll
+  for (int t = 0; t < tab.n; ++t) {
+    float term = tab.coef[t];
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+      for (int q = 0; q < tab.k[t][j]; ++q) term *= c.pk[j];
+    e += term;
+  }
+  E = e;
+}
 template <> __device__ __forceinline__ void acc_final<2>(const Acc<2>& c, float& A, float& B, float& E) {
   const float P1 = c.pa.x, P2 = c.pb.x;
   A = c.pa.y; B = c.pb.y;
@@ -270,7 +351,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
 template <int P, int KM>
-__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : 2)) k_beamform(const BeamformArgs a) {
+__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;
@@ -353,7 +434,10 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W) {
   if ((e = configure_order<2>(bytes))) return e;
   if ((e = configure_order<3>(bytes))) return e;
   if ((e = configure_order<4>(bytes))) return e;
-  return configure_order<5>(bytes);
+  if ((e = configure_order<5>(bytes))) return e;
+  if ((e = configure_order<6>(bytes))) return e;
+  if ((e = configure_order<7>(bytes))) return e;
+  return configure_order<8>(bytes);
 }
 
 template <int P>
@@ -373,6 +457,9 @@ cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, 
     case 3: launch_order<3>(a, grid, smem, st); break;
     case 4: launch_order<4>(a, grid, smem, st); break;
     case 5: launch_order<5>(a, grid, smem, st); break;
+    case 6: launch_order<6>(a, grid, smem, st); break;
+    case 7: launch_order<7>(a, grid, smem, st); break;
+    case 8: launch_order<8>(a, grid, smem, st); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -208,8 +208,10 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->n_samples > ((int64_t)1 << 30)) return fail(DMAS_ERR_INVALID, "n_samples too large");
   if (!(d->fs_hz > 0) || !std::isfinite(d->fs_hz)) return fail(DMAS_ERR_INVALID, "fs_hz must be > 0");
   if (!(d->c_mps > 0) || !std::isfinite(d->c_mps)) return fail(DMAS_ERR_INVALID, "c_mps must be > 0");
-  if (d->order < 2 || d->order > 5) return fail(DMAS_ERR_ORDER, "order must be in [2,5]");
+  if (d->order < 2 || d->order > 8) return fail(DMAS_ERR_ORDER, "order must be in [2,8]");
   if (d->n_mics < d->order) return fail(DMAS_ERR_ORDER, "n_mics < order (N < n)");
+  if (d->order > 5 && d->n_mics < 2 * d->order)
+    return fail(DMAS_ERR_ORDER, "orders 6..8 need n_mics >= 2p (fp32 Newton-Girard cancellation)");
   if (d->max_frames < 1 || d->max_frames > 65535) return fail(DMAS_ERR_INVALID, "max_frames not in [1,65535]");
   if (!(d->cf_eps >= 0.0f) || !std::isfinite(d->cf_eps)) return fail(DMAS_ERR_INVALID, "cf_eps must be >= 0");
   if (d->lp_taps < 0 || (d->lp_taps > 0 && d->lp_taps % 2 == 0) || d->lp_taps > 4095)

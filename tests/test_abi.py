@@ -74,8 +74,10 @@ def _plan_err(dm, **kw):
 
 def test_validation_errors(dm):
     """Host-side validation (include/dmas.h DMAS_ERR_*) happens before any CUDA call."""
-    assert _plan_err(dm, order=6) == 3
+    assert _plan_err(dm, order=9) == 3
     assert _plan_err(dm, order=1) == 3
+    twelve = np.stack([np.zeros(11), 0.004 * np.arange(11), np.zeros(11)], axis=1)
+    assert _plan_err(dm, order=6, mic_xyz=twelve) == 3     # p >= 6 needs n_mics >= 2p
     assert _plan_err(dm, order=4) == 3                      # n_mics (3) < p  (SPEC "N < n")
     assert _plan_err(dm, c=0.0) == 2
     assert _plan_err(dm, fs=-1.0) == 2

@@ -390,3 +390,29 @@ def test_matched_filter_host_path_and_validation(dm):
         plan.beamform(torch.zeros((1, 8, cfg["T"]), device="cuda"), what)
     with pytest.raises(dm.DmasError):
         dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], mf_coeffs=np.zeros(16))
+
+
+# ------------------------------------------------------------------ NEXT-3: orders 6..8 (general partition formula)
+@pytest.mark.parametrize("p", [6, 7, 8])
+def test_high_orders_config_C3(dm, p):
+    """Orders 6..8 through the general Newton-Girard partition formula on the C3
+    scene (32 mics >= 2p), every kind raw + envelope, against the oracle's Vieta E_p."""
+    cfg = gen.config("C3")
+    dirs = cfg["dirs"][::3]
+    plan, g = run_gpu(dm, cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, cfg["signals"], what_all(dm))
+    ref = oracle_images(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, cfg["signals"], env_kinds=KINDS)
+    for key in ref:
+        assert_parity(g[key], ref[key], f"C3 p={p} {key}")
+
+
+@pytest.mark.parametrize("p", [6, 7, 8])
+def test_high_orders_slice_bruteforce(dm, p):
+    """Broadside slice harness: random slices of N = 2p microphones against Eq. (5) brute force."""
+    import torch
+    rng = np.random.default_rng(80 + p)
+    n, T = 2 * p, 200
+    x = rng.uniform(-1, 1, (n, T)).astype(np.float32)
+    plan = _slice_plan(dm, n, p, T)
+    g = plan.beamform(torch.from_numpy(x[None]).cuda(), dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
+    ref = np.array([O.brute_force_esp(list(O.signed_root(x[:, t].astype(np.float64), p)), p) for t in range(T)])
+    assert np.max(np.abs(g - ref)) <= TOL * np.max(np.abs(ref))
