@@ -29,6 +29,7 @@ from .dmas_oracle import (  # noqa: F401
     envelope,
     esp_vieta,
     gather,
+    gather_linear,
     lpf_taps,
     matched_filter,
     newton_girard_explicit,

@@ -42,7 +42,7 @@ def unit_vector(az: float, el: float):
     return (ce * math.cos(az), ce * math.sin(az), math.sin(el))
 
 
-def delay_table(mic_xyz, dir_az_el, fs: float, c: float, reference=None, return_exact=False):
+def delay_table(mic_xyz, dir_az_el, fs: float, c: float, reference=None, return_exact=False, mode="nearest"):
     """Integer-sample delay LUT d[psi][i] ("pre-computed and stored in
     a delay matrix look-up table").
 
@@ -56,6 +56,8 @@ def delay_table(mic_xyz, dir_az_el, fs: float, c: float, reference=None, return_
         v   = dot * k,   k = -(fs / c)
 
     Returns int32 [n_dirs][n_mics] (and the exact float v if ``return_exact``).
+    ``mode="linear"`` (NEXT-2, reading Q4b): returns (d0, alpha) with d0 = floor(v) (int32) and
+    alpha = v - d0 in [0, 1) (float64) for linear-interpolation pre-steering.
     """
     mic_xyz = np.asarray(mic_xyz, dtype=np.float64)
     dir_az_el = np.asarray(dir_az_el, dtype=np.float64)
@@ -67,16 +69,18 @@ def delay_table(mic_xyz, dir_az_el, fs: float, c: float, reference=None, return_
     k = -(float(fs) / float(c))
     n_dirs, n_mics = dir_az_el.shape[0], mic_xyz.shape[0]
     d = np.empty((n_dirs, n_mics), dtype=np.int32)
-    v_exact = np.empty((n_dirs, n_mics), dtype=np.float64) if return_exact else None
+    v_exact = np.empty((n_dirs, n_mics), dtype=np.float64) if (return_exact or mode == "linear") else None
     mics = [tuple(float(q) for q in row) for row in mic_xyz]
     for a in range(n_dirs):
         ux, uy, uz = unit_vector(float(dir_az_el[a, 0]), float(dir_az_el[a, 1]))
         for i, (px, py, pz) in enumerate(mics):
             dot = ((px - rx) * ux + (py - ry) * uy) + (pz - rz) * uz
             v = dot * k
-            d[a, i] = round(v)
-            if return_exact:
+            d[a, i] = round(v) if mode == "nearest" else math.floor(v)
+            if return_exact or mode == "linear":
                 v_exact[a, i] = v
+    if mode == "linear":
+        return d, v_exact - d
     return (d, v_exact) if return_exact else d
 
 
@@ -119,6 +123,18 @@ def gather(m, d):
             if lo < hi:
                 x[a, i, lo:hi] = m[i, lo + s:hi + s]
     return x
+
+
+def gather_linear(m, d0, alpha):
+    """Fractional-delay pre-steering by linear interpolation (Eq. (1) PAPER.md:79 with a
+    non-integer delay; reading Q4b, "fractional-sample interpolation"):
+    x_i(t, psi) = (1 - a) m_i[t + d0] + a m_i[t + d0 + 1], a = alpha[psi][i]; samples outside
+    [0, T) are 0.  Returns float64 [n_dirs][n_mics][T]."""
+    m = np.asarray(m, dtype=np.float64)
+    lo = gather(m, d0)
+    hi = gather(m, np.asarray(d0, dtype=np.int64) + 1)
+    a = np.asarray(alpha, dtype=np.float64)[:, :, None]
+    return (1.0 - a) * lo + a * hi
 
 
 # --------------------------------------------------------------------------------------
@@ -247,12 +263,13 @@ def coherence_factor(A, B, n_mics: int, eps: float = 1e-30):
     return (A * A) / (n_mics * B + eps)
 
 
-def beamform_frame(m, d, p: int, eps: float = 1e-30, chunk: int = 32):
+def beamform_frame(m, d, p: int, eps: float = 1e-30, chunk: int = 32, alpha=None):
     """All raw images of one frame: DAS (Eq. (2)), DMAS_p (Eqs. (5)/(6)
     PAPER.md:106/116 via ``esp_vieta``), CF, CF-DMAS
     (PAPER.md:177), CF-DAS (PAPER.md:179 "can also be applied to DAS").
 
-    ``m``: [n_mics][T] (fp32 input promoted to float64), ``d``: [n_dirs][n_mics].
+    ``m``: [n_mics][T] (fp32 input promoted to float64), ``d``: [n_dirs][n_mics]; with
+    ``alpha`` (NEXT-2) the pre-steering interpolates linearly between d and d + 1.
     Returns dict kind -> float64 [n_dirs][T].
     """
     m = np.asarray(m, dtype=np.float64)
@@ -262,7 +279,7 @@ def beamform_frame(m, d, p: int, eps: float = 1e-30, chunk: int = 32):
     out = {k: np.empty((n_dirs, T), dtype=np.float64) for k in KIND_NAMES}
     for a0 in range(0, n_dirs, chunk):
         a1 = min(n_dirs, a0 + chunk)
-        x = gather(m, d[a0:a1])                       # [dirs][mics][T]
+        x = gather(m, d[a0:a1]) if alpha is None else gather_linear(m, d[a0:a1], alpha[a0:a1])
         A = np.sum(x, axis=1)                         # Eq. (2)
         B = np.sum(x * x, axis=1)                     # CF denominator
         s = signed_root(x, p)

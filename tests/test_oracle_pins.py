@@ -399,3 +399,40 @@ def test_matched_filter_definition_and_library_cases():
     r = gen.raw_frame(mic, [(0.3, 0.1, 0.6, 1.0)], 800, snr_db=0.0, seed=1)
     np.testing.assert_allclose(O.matched_filter(r, gen.chirp_samples(), 800), gen.matched_filter(r, 800),
                                rtol=1e-9, atol=1e-9)
+
+
+# ----------------------------------------------------------------- NEXT-2 fractional-delay pre-steering
+def test_linear_delay_table_and_gather():
+    """d0 = floor(v), alpha = v - d0 in [0,1), d0 + alpha = the exact delay; alpha = 0 reduces to the
+    integer gather; linear interpolation reproduces a linear ramp exactly; alpha = 1/2 averages."""
+    mic = gen.disk_array(16, seed=3)
+    dirs = gen.az_el_grid(7, 70.0, 5, 40.0)
+    d0, al = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, mode="linear")
+    _, v = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, return_exact=True)
+    assert np.all((al >= 0) & (al < 1))
+    np.testing.assert_allclose(d0 + al, v, rtol=0, atol=1e-12)
+    assert np.array_equal(d0, np.floor(v).astype(np.int32))
+    rng = np.random.default_rng(90)
+    m = rng.standard_normal((16, 300))
+    np.testing.assert_array_equal(O.gather_linear(m, d0, np.zeros_like(al)), O.gather(m, d0))
+    ramp = np.tile(0.25 * np.arange(300.0) - 3.0, (16, 1))
+    x = O.gather_linear(ramp, d0, al)
+    t = np.arange(300.0)
+    inside = (t[None, None, :] + d0[:, :, None] >= 0) & (t[None, None, :] + d0[:, :, None] + 1 < 300)
+    exp = 0.25 * (t[None, None, :] + d0[:, :, None] + al[:, :, None]) - 3.0
+    np.testing.assert_allclose(x[inside], exp[inside], rtol=1e-12, atol=1e-12)
+    half = O.gather_linear(m, d0, np.full_like(al, 0.5))
+    np.testing.assert_allclose(half, 0.5 * (O.gather(m, d0) + O.gather(m, d0 + 1)), rtol=1e-13)
+
+
+def test_linear_presteer_aligns_physical_plane_wave():
+    """A fractional plane wave (analytic echoes at non-integer delays) is aligned better by linear
+    interpolation than by nearest-sample steering: higher CF at the echo (SPEC.md:217 rationale)."""
+    mic = gen.disk_array(32, seed=7)
+    az, el = math.radians(17.0), math.radians(-9.0)
+    m = gen.frame(mic, [(az, el, 0.5, 1.0)], 1536)
+    d = O.delay_table(mic, [[az, el]], gen.FS, gen.C_SOUND)
+    d0, al = O.delay_table(mic, [[az, el]], gen.FS, gen.C_SOUND, mode="linear")
+    cf_near = O.beamform_frame(m, d, 2)["cf"][0, 1300:1325].max()
+    cf_lin = O.beamform_frame(m, d0, 2, alpha=al)["cf"][0, 1300:1325].max()
+    assert cf_lin > cf_near > 0.5
