@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--workload", choices=["C5", "C4"], default="C5",
                     help="C5 = the metric's config (default); C4 = 64-mic p = 3 secondary line")
     ap.add_argument("--mode", choices=["weak", "dirshard"], default="weak")
+    ap.add_argument("--interp", action="store_true",
+                    help="linear-interpolation pre-steering (fractional delays, roots on the fly; NEXT-2)")
     ap.add_argument("--raw", action="store_true",
                     help="raw recordings in: the step includes the GPU matched filter (paper Fig. 1 pipeline)")
     ap.add_argument("--e2e-frames", type=int, default=16)
@@ -174,7 +176,8 @@ def config_dict(args, world):
             "outputs": f"CF-DMAS{w['order']} envelope (127-tap 5 kHz low-pass)",
             "mode": args.mode, "world": world, "l2": w["l2"],
             "input": "raw recordings, matched filter on the GPU (1125-tap chirp)" if args.raw
-                     else "matched-filtered signals (north_star input)"}
+                     else "matched-filtered signals (north_star input)",
+            "presteer": "linear interpolation (fractional delays)" if args.interp else "nearest sample (integer LUT)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -260,7 +263,7 @@ def run_ours(args, rank, world, local):
             x.copy_(torch.from_numpy(cfg["signals"]))
     F, T, p = args.frames, cfg["T"], cfg["order"]
     plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, max_frames=F, lp_taps=LP_TAPS, device=local,
-                     mf_coeffs=cfg.get("chirp") if args.raw else None)
+                     mf_coeffs=cfg.get("chirp") if args.raw else None, delay_interp=1 if args.interp else 0)
     what = dmas.ENV(dmas.KIND_CFDMAS)
     out = torch.empty((F, len(dirs), T), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()

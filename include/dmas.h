@@ -98,6 +98,11 @@ typedef struct {
      (an exact unit echo starting at sample t peaks at 1 at t).  0 = signals are matched-filtered. */
   int32_t mf_taps;           /* 0 (default) or 1..16384                                         */
   const float* mf_coeffs;    /* [mf_taps] host, copied (the emitted chirp)                      */
+  /* Pre-steering of Eq. (1) with a fractional delay (NEXT-2): 0 = nearest sample,
+     ties to even (default; the integer LUT north_star names); 1 = linear interpolation,
+     x_i(t) = (1 - a) m_i(t + d) + a m_i(t + d + 1) with d = floor(v), a = v - d (SPEC's
+     pre_steer); roots are then taken per pixel on the SFU instead of hoisted.                  */
+  int32_t delay_interp;
   /* Runtime. */
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an
@@ -136,8 +141,13 @@ dmas_status dmas_beamform(dmas_plan_t plan, const float* signals, int32_t n_fram
 dmas_status dmas_beamform_host(dmas_plan_t plan, const float* host_signals, int32_t n_frames,
                                float* const* host_outs, uint32_t what);
 
-/* Copy the plan's integer delay table into host memory int32 [n_dirs][n_mics]. */
+/* Copy the plan's integer delay table into host memory int32 [n_dirs][n_mics] (nearest sample,
+   or floor(v) when delay_interp == 1). */
 dmas_status dmas_delay_table(dmas_plan_t plan, int32_t* host_out);
+
+/* delay_interp == 1 plans only: the fractional parts a = v - floor(v) in [0, 1), fp32
+   [n_dirs][n_mics]; DMAS_ERR_SHAPE for nearest-sample plans. */
+dmas_status dmas_delay_fraction(dmas_plan_t plan, float* host_out);
 
 typedef struct {
   int64_t n_dirs, n_samples, n_out_samples; /* n_out_samples = ceil(T / env_decim)            */

@@ -25,7 +25,8 @@ namespace dmas {
 //   dot = ((px - rx)*ux + (py - ry)*uy) + (pz - rz)*uz ;  v = dot * k ;  d = rint_even(v)
 // ------------------------------------------------------------------------------------------
 __global__ void k_delay_table(const double* __restrict__ u, const double* __restrict__ pos, double rx, double ry,
-                              double rz, double k, int64_t n_dirs, int32_t n_mics, int32_t* __restrict__ out) {
+                              double rz, double k, int64_t n_dirs, int32_t n_mics, int32_t* __restrict__ out,
+                              float* __restrict__ alpha) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_dirs * (int64_t)n_mics) return;
   const int64_t a = idx / n_mics;
@@ -34,15 +35,21 @@ __global__ void k_delay_table(const double* __restrict__ u, const double* __rest
   const double dx = __dsub_rn(pos[3 * i], rx), dy = __dsub_rn(pos[3 * i + 1], ry), dz = __dsub_rn(pos[3 * i + 2], rz);
   const double dot = __dadd_rn(__dadd_rn(__dmul_rn(dx, ux), __dmul_rn(dy, uy)), __dmul_rn(dz, uz));
   const double v = __dmul_rn(dot, k);
-  out[idx] = __double2int_rn(v);
+  if (alpha) {                                       // linear pre-steering: floor + fraction
+    const int d0 = __double2int_rd(v);
+    out[idx] = d0;
+    alpha[idx] = (float)__dsub_rn(v, (double)d0);
+  } else {
+    out[idx] = __double2int_rn(v);
+  }
 }
 
 cudaError_t launch_delay_table(const double* u, const double* pos, double rx, double ry, double rz, double k,
-                               int64_t n_dirs, int32_t n_mics, int32_t* out, cudaStream_t st) {
+                               int64_t n_dirs, int32_t n_mics, int32_t* out, float* alpha, cudaStream_t st) {
   const int64_t n = n_dirs * (int64_t)n_mics;
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
-  k_delay_table<<<(unsigned)blocks, threads, 0, st>>>(u, pos, rx, ry, rz, k, n_dirs, n_mics, out);
+  k_delay_table<<<(unsigned)blocks, threads, 0, st>>>(u, pos, rx, ry, rz, k, n_dirs, n_mics, out, alpha);
   return cudaGetLastError();
 }
 
@@ -52,6 +59,7 @@ cudaError_t launch_delay_table(const double* u, const double* pos, double rx, do
 // ------------------------------------------------------------------------------------------
 template <int P>
 __device__ __forceinline__ float signed_root(float v) {
+  if (P == 1) return v;                              // identity plane (interpolating path)
   const float a = fabsf(v);
   float r;
   if (P == 2) r = __fsqrt_rn(a);
@@ -79,6 +87,7 @@ cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t row
   if (bx > 64) bx = 64;
   dim3 grid((unsigned)rows, (unsigned)bx);
   switch (order) {
+    case 1: k_signed_roots<1><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     case 2: k_signed_roots<2><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     case 3: k_signed_roots<3><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
     case 4: k_signed_roots<4><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
@@ -142,6 +151,7 @@ cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const fl
   dim3 grid((unsigned)rows, (unsigned)((T + MF_T - 1) / MF_T));
   const size_t smem = (size_t)(2 * Lp + MF_T) * sizeof(float);
   switch (order) {
+    case 1: k_mf_roots<1><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     case 2: k_mf_roots<2><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     case 3: k_mf_roots<3><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
     case 4: k_mf_roots<4><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
@@ -157,6 +167,7 @@ cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const fl
 cudaError_t mf_configure(int32_t Lp) {
   const int smem = (2 * Lp + MF_T) * (int)sizeof(float);
   cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_mf_roots<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(k_mf_roots<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(k_mf_roots<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(k_mf_roots<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
@@ -342,6 +353,33 @@ template <> __device__ __forceinline__ void acc_final<5>(const Acc<5>& c, float&
        30.f * P1 * P4 + 24.f * P5) * (1.f / 120.f);
 }
 
+// Signed root of an interpolated sample, on the fly (SFU approximations, rel. error ~2^-22).
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+template <int P>
+__device__ __forceinline__ float root_fast(float x) {
+  const float a = fabsf(x);
+  float r;
+  if (P == 2) r = sqrt_approx(a);
+  else if (P == 4) r = sqrt_approx(sqrt_approx(a));
+  else if (P == 8) r = sqrt_approx(sqrt_approx(sqrt_approx(a)));
+  else r = ex2_approx(lg2_approx(a) * (1.0f / (float)P));     // lg2(0) = -inf -> ex2 = +0
+  return copysignf(r, x);
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -350,13 +388,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
-template <int P, int KM>
+// INTERP (NEXT-2): the window holds m (not roots); per (psi, mic) a fraction alpha in [0, 1):
+// x = m[j] + alpha (m[j + 1] - m[j]), roots on the fly on the SFU.
+template <int P, int KM, bool INTERP>
 __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;
   float* win = smem;                                   // [n_mics][W]   staged S window
   int32_t* offs = reinterpret_cast<int32_t*>(smem + (size_t)n_mics * W);  // [BF_PSI][n_mics]
+  float* alph = reinterpret_cast<float*>(offs + BF_PSI * n_mics);        // [BF_PSI][n_mics] (INTERP)
 
   const int64_t t0 = (int64_t)blockIdx.x * BF_T;
   const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
@@ -379,7 +420,10 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   // delay rows of this psi tile -> smem word offsets into the window (overlaps the TMA)
   for (int q = warp; q < npsi; q += BF_WARPS) {
     const int32_t* drow = a.delays + (psi0 + q) * n_mics;
-    for (int i = lane; i < n_mics; i += 32) offs[q * n_mics + i] = i * W + (__ldg(drow + i) - lo);
+    for (int i = lane; i < n_mics; i += 32) {
+      offs[q * n_mics + i] = i * W + (__ldg(drow + i) - lo);
+      if (INTERP) alph[q * n_mics + i] = __ldg(a.alpha + (psi0 + q) * n_mics + i);
+    }
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -391,11 +435,25 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
     const int32_t* oq = offs + q * n_mics;
+    if (INTERP) {
+      const float* aq = alph + q * n_mics;
 #pragma unroll BF_UNROLL
-    for (int i = 0; i < n_mics; ++i) {
-      const float* w = wl + oq[i];
+      for (int i = 0; i < n_mics; ++i) {
+        const float* w = wl + oq[i];
+        const float al = aq[i];
 #pragma unroll
-      for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
+        for (int k = 0; k < BF_KT; ++k) {
+          const float m0 = w[32 * k], m1 = w[32 * k + 1];
+          acc_add<P>(acc[k], root_fast<P>(fmaf(al, m1 - m0, m0)));
+        }
+      }
+    } else {
+#pragma unroll BF_UNROLL
+      for (int i = 0; i < n_mics; ++i) {
+        const float* w = wl + oq[i];
+#pragma unroll
+        for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
+      }
     }
     const int64_t o = (f * a.n_dirs + psi0 + q) * a.T + t0 + lane;
 #pragma unroll
@@ -417,19 +475,21 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   }
 }
 
-size_t beamform_smem_bytes(int32_t n_mics, int32_t W) {
-  return (size_t)n_mics * W * sizeof(float) + (size_t)BF_PSI * n_mics * sizeof(int32_t);
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp) {
+  return (size_t)n_mics * W * sizeof(float) + (size_t)BF_PSI * n_mics * (interp ? 8 : 4);
 }
 
 template <int P>
 static cudaError_t configure_order(int bytes) {
-  cudaError_t e = cudaFuncSetAttribute(k_beamform<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_beamform<P, 31>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform<P, 31, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-cudaError_t beamform_configure(int32_t n_mics, int32_t W) {
-  const int bytes = (int)beamform_smem_bytes(n_mics, W);
+cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp) {
+  const int bytes = (int)beamform_smem_bytes(n_mics, W, interp);
   cudaError_t e;
   if ((e = configure_order<2>(bytes))) return e;
   if ((e = configure_order<3>(bytes))) return e;
@@ -443,15 +503,20 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W) {
 template <int P>
 static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
-  if (only_cfdmas) k_beamform<P, 4><<<grid, BF_THREADS, smem, st>>>(a);
-  else k_beamform<P, 31><<<grid, BF_THREADS, smem, st>>>(a);
+  if (a.alpha) {
+    if (only_cfdmas) k_beamform<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
+    else k_beamform<P, 31, true><<<grid, BF_THREADS, smem, st>>>(a);
+  } else {
+    if (only_cfdmas) k_beamform<P, 4, false><<<grid, BF_THREADS, smem, st>>>(a);
+    else k_beamform<P, 31, false><<<grid, BF_THREADS, smem, st>>>(a);
+  }
 }
 
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
   const int64_t ntt = (a.T + BF_T - 1) / BF_T;
   const int64_t npt = (a.n_dirs + BF_PSI - 1) / BF_PSI;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = beamform_smem_bytes(a.n_mics, a.W);
+  const size_t smem = beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;
     case 3: launch_order<3>(a, grid, smem, st); break;

@@ -46,6 +46,7 @@ struct BeamformArgs {
   const int32_t* delays;    // [n_dirs][n_mics] int32 sample delays d[psi][i]
   const int32_t* tile_lo;   // [n_psi_tiles] window origin (relative to t0) of each psi tile, %4 == 0
   float* out[N_KINDS];      // raw-image destinations [frames][n_dirs][T] (nullptr = kind not written)
+  const float* alpha;       // [n_dirs][n_mics] fractional delays in [0, 1) (linear pre-steering), or null
   int64_t Tp, G, T, n_dirs;
   int32_t n_mics, W;        // W = staged samples per mic row (multiple of 4)
   float n_mics_f, cf_eps;
@@ -54,11 +55,13 @@ struct BeamformArgs {
 struct LpTaps127 { float h[128]; };
 
 // K1: d[psi][i] = rint_even(((p_i - r) . u_psi) * k) in IEEE fp64, no contraction (A1).
+// With `alpha` non-null (linear pre-steering, NEXT-2): d = floor(v) and alpha = v - d (fp32).
 cudaError_t launch_delay_table(const double* u /*[n_dirs][3]*/, const double* pos /*[n_mics][3]*/,
                                double rx, double ry, double rz, double k, int64_t n_dirs, int32_t n_mics,
-                               int32_t* out, cudaStream_t st);
+                               int32_t* out, float* alpha, cudaStream_t st);
 
-// K2: S[f][i][G + t] = sgn(m) |m|^(1/p) for t in [0, T) (hoisted signed roots, A3).
+// K2: S[f][i][G + t] = sgn(m) |m|^(1/p) for t in [0, T) (hoisted signed roots, A3); order 1 =
+// identity (the plane of m itself, used by the interpolating beamformer).
 cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp,
                                 int64_t G, cudaStream_t st);
 
@@ -70,8 +73,8 @@ cudaError_t mf_configure(int32_t Lp);
 
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
-size_t beamform_smem_bytes(int32_t n_mics, int32_t W);
-cudaError_t beamform_configure(int32_t n_mics, int32_t W);   // opt-in to > 48 KB dynamic smem
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp);
+cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp);   // opt-in to > 48 KB dynamic smem
 
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).
 cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,

@@ -76,6 +76,9 @@ struct dmas_plan_s {
   int32_t mf_taps = 0, mf_lp = 0;     // matched filter taps / padded to a multiple of 4
   float mf_inv_energy = 0.f;
   float* d_mf = nullptr;
+  bool interp = false;                // linear-interpolation pre-steering (NEXT-2)
+  float* d_alpha = nullptr;           // [n_dirs][n_mics] fractional delays
+  std::vector<float> h_alpha;
   double fs = 0, c = 0;
   float cf_eps = 1e-30f;
   int32_t dmin = 0, dmax = 0;
@@ -158,6 +161,7 @@ void free_plan_memory(dmas_plan_s* p) {
   cudaFree(p->d_lp);
   cudaFree(p->d_bp);
   cudaFree(p->d_mf);
+  cudaFree(p->d_alpha);
   cudaFree(p->d_scratch);
   for (int b = 0; b < 2; ++b) {
     cudaFree(p->d_hsig[b]);
@@ -225,6 +229,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
   if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
+  if (d->delay_interp < 0 || d->delay_interp > 1) return fail(DMAS_ERR_INVALID, "delay_interp not in {0, 1}");
   if (d->mf_taps < 0 || d->mf_taps > dmas::MF_MAX_TAPS) return fail(DMAS_ERR_INVALID, "mf_taps not in [0, 16384]");
   if (d->mf_taps > 0 && !d->mf_coeffs) return fail(DMAS_ERR_NULL, "mf_coeffs is NULL");
   if (d->mf_taps > 0) {
@@ -263,18 +268,20 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   if (wait_env) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[pp], 0));
   if (p->mf_taps > 0) {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
-      return dmas::launch_mf_roots(p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
+      return dmas::launch_mf_roots(p->interp ? 1 : p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
                                    (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
     }));
   } else {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
-      return dmas::launch_signed_roots(p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
+      return dmas::launch_signed_roots(p->interp ? 1 : p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T,
+                                       p->Tp, p->G, st);
     }));
   }
   dmas::BeamformArgs a{};
   a.splane = p->d_splane;
   a.delays = p->d_delays;
   a.tile_lo = p->d_tile_lo;
+  a.alpha = p->interp ? p->d_alpha : nullptr;
   for (int k = 0; k < dmas::N_KINDS; ++k) a.out[k] = raw_dst[k];
   a.Tp = p->Tp;
   a.G = p->G;
@@ -483,12 +490,19 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   PLAN_TRY(cudaMalloc(&d_u, u.size() * sizeof(double)));
   PLAN_TRY(cudaMalloc(&d_pos, (size_t)nm * 3 * sizeof(double)));
   PLAN_TRY(cudaMalloc(&p->d_delays, (size_t)nd * nm * sizeof(int32_t)));
+  p->interp = desc->delay_interp == 1;
+  if (p->interp) PLAN_TRY(cudaMalloc(&p->d_alpha, (size_t)nd * nm * sizeof(float)));
   PLAN_TRY(cudaMemcpy(d_u, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice));
   PLAN_TRY(cudaMemcpy(d_pos, desc->mic_xyz, (size_t)nm * 3 * sizeof(double), cudaMemcpyHostToDevice));
   PLAN_TRY(timed(p, K_DELAY, nullptr,
-                 [&] { return dmas::launch_delay_table(d_u, d_pos, rx, ry, rz, k, nd, nm, p->d_delays, nullptr); }));
+                 [&] { return dmas::launch_delay_table(d_u, d_pos, rx, ry, rz, k, nd, nm, p->d_delays, p->d_alpha,
+                                                       nullptr); }));
   p->h_delays.resize((size_t)nd * nm);
   PLAN_TRY(cudaMemcpy(p->h_delays.data(), p->d_delays, p->h_delays.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (p->interp) {
+    p->h_alpha.resize((size_t)nd * nm);
+    PLAN_TRY(cudaMemcpy(p->h_alpha.data(), p->d_alpha, p->h_alpha.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  }
   cudaFree(d_u);
   cudaFree(d_pos);
 
@@ -513,16 +527,16 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     tile_lo[(size_t)t] = lo_al;
     lo_min = std::min(lo_min, lo_al);
     lo_max = std::max(lo_max, lo_al);
-    wmax = std::max(wmax, dmas::BF_T + (hi - lo_al));
+    wmax = std::max(wmax, dmas::BF_T + (hi - lo_al) + (p->interp ? 1 : 0));   // + m[j + 1] when interpolating
   }
   p->W = (wmax + 3) / 4 * 4;
-  const size_t smem = dmas::beamform_smem_bytes(nm, p->W);
+  const size_t smem = dmas::beamform_smem_bytes(nm, p->W, p->interp);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (smem + 64 > (size_t)smem_optin)
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
-  PLAN_TRY(dmas::beamform_configure(nm, p->W));
+  PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp));
   PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
   PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
 
@@ -687,6 +701,13 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
 dmas_status dmas_delay_table(dmas_plan_t p, int32_t* host_out) {
   if (!p || !host_out) return fail(DMAS_ERR_NULL, "NULL argument");
   std::memcpy(host_out, p->h_delays.data(), p->h_delays.size() * sizeof(int32_t));
+  return DMAS_OK;
+}
+
+dmas_status dmas_delay_fraction(dmas_plan_t p, float* host_out) {
+  if (!p || !host_out) return fail(DMAS_ERR_NULL, "NULL argument");
+  if (!p->interp) return fail(DMAS_ERR_SHAPE, "plan uses nearest-sample delays (delay_interp == 0)");
+  std::memcpy(host_out, p->h_alpha.data(), p->h_alpha.size() * sizeof(float));
   return DMAS_OK;
 }
 

@@ -61,6 +61,7 @@ class dmas_plan_desc(ctypes.Structure):
         ("env_engine", ctypes.c_int32),
         ("mf_taps", ctypes.c_int32),
         ("mf_coeffs", ctypes.POINTER(ctypes.c_float)),
+        ("delay_interp", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
     ]
@@ -78,6 +79,7 @@ class dmas_plan_info(ctypes.Structure):
 
 # The exported C symbols (include/dmas.h).  tests/test_abi.py checks the .so exports each.
 EXPORTS = ("dmas_plan_desc_init", "dmas_plan", "dmas_beamform", "dmas_beamform_host", "dmas_delay_table",
+           "dmas_delay_fraction",
            "dmas_get_plan_info", "dmas_set_timing", "dmas_timing_read", "dmas_launch_count", "dmas_destroy",
            "dmas_status_string", "dmas_last_error")
 
@@ -98,6 +100,8 @@ def _load() -> ctypes.CDLL:
     lib.dmas_beamform_host.restype = ctypes.c_int
     lib.dmas_delay_table.argtypes = [P, P]
     lib.dmas_delay_table.restype = ctypes.c_int
+    lib.dmas_delay_fraction.argtypes = [P, P]
+    lib.dmas_delay_fraction.restype = ctypes.c_int
     lib.dmas_get_plan_info.argtypes = [P, ctypes.POINTER(dmas_plan_info)]
     lib.dmas_get_plan_info.restype = ctypes.c_int
     lib.dmas_set_timing.argtypes = [P, ctypes.c_int32]
@@ -146,7 +150,7 @@ class Plan:
                  max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
                  device: int = -1, scratch_bytes: int = 0, env_engine: int = 0,
-                 mf_coeffs: Optional[Sequence[float]] = None):
+                 mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -170,6 +174,7 @@ class Plan:
             d.bp_coeffs = bp.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         d.env_decim, d.device, d.scratch_bytes = int(env_decim), int(device), int(scratch_bytes)
         d.env_engine = int(env_engine)
+        d.delay_interp = int(delay_interp)
         self.mf_taps = 0
         if mf_coeffs is not None and len(mf_coeffs) > 0:
             mf = np.ascontiguousarray(np.asarray(mf_coeffs, dtype=np.float32))
@@ -190,6 +195,12 @@ class Plan:
     def delay_table(self) -> np.ndarray:
         out = np.empty((self.n_dirs, self.n_mics), dtype=np.int32)
         _check(lib.dmas_delay_table(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    # -- dmas_delay_fraction (linear pre-steering plans)
+    def delay_fraction(self) -> np.ndarray:
+        out = np.empty((self.n_dirs, self.n_mics), dtype=np.float32)
+        _check(lib.dmas_delay_fraction(self._h, out.ctypes.data_as(ctypes.c_void_p)))
         return out
 
     def out_shapes(self, n_frames: int, what: int):

@@ -416,3 +416,46 @@ def test_high_orders_slice_bruteforce(dm, p):
     g = plan.beamform(torch.from_numpy(x[None]).cuda(), dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
     ref = np.array([O.brute_force_esp(list(O.signed_root(x[:, t].astype(np.float64), p)), p) for t in range(T)])
     assert np.max(np.abs(g - ref)) <= TOL * np.max(np.abs(ref))
+
+
+# ------------------------------------------------------------------ NEXT-2: linear-interpolation pre-steering
+@pytest.mark.parametrize("name,p", [("C1", 2), ("C2", 2), ("C3", 3), ("C3", 5)])
+def test_linear_presteer_parity(dm, name, p):
+    """delay_interp = 1: floor table bit-exact, fractions to fp32 rounding, every kind raw + envelope
+    against the oracle's gather_linear -> beamform_frame."""
+    cfg = gen.config(name)
+    dirs = cfg["dirs"] if name == "C1" else cfg["dirs"][::2]
+    plan, g = run_gpu(dm, cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, cfg["signals"], what_all(dm), delay_interp=1)
+    d0, al = O.delay_table(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], mode="linear")
+    assert np.array_equal(plan.delay_table(), d0)
+    assert np.max(np.abs(plan.delay_fraction() - al)) <= 6e-8
+    ref = {}
+    h = O.lpf_taps()
+    img = O.beamform_frame(cfg["signals"][0], d0, p, alpha=al)
+    for k in KINDS:
+        ref[("raw", k)] = img[k][None]
+        ref[("env", k)] = O.envelope(img[k], h)[None]
+    for key in ref:
+        assert_parity(g[key], ref[key], f"linear {name} p={p} {key}")
+
+
+def test_linear_presteer_with_matched_filter_and_slices(dm):
+    """Linear pre-steering composed with the GPU matched filter; and the broadside slice harness
+    (all fractions 0) reproduces the integer path's brute-force values."""
+    import torch
+    cfg = gen.raw_config("C1", frames=1)
+    plan, g = run_gpu(dm, cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["signals"],
+                      dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS), n_samples=cfg["T"], mf_coeffs=cfg["chirp"],
+                      delay_interp=1)
+    mf = O.matched_filter(cfg["signals"][0], cfg["chirp"], cfg["T"])
+    d0, al = O.delay_table(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], mode="linear")
+    img = O.beamform_frame(mf, d0, 2, alpha=al)
+    assert_parity(g[("raw", "cfdmas")], img["cfdmas"][None], "MF+linear raw")
+    assert_parity(g[("env", "cfdmas")], O.envelope(img["cfdmas"], O.lpf_taps())[None], "MF+linear env")
+    x = np.random.default_rng(91).uniform(-1, 1, (7, 64)).astype(np.float32)
+    mic = np.stack([np.zeros(7), 0.003 * np.arange(7), np.zeros(7)], axis=1)
+    plan = dm.Plan(mic, [[0.0, 0.0]], gen.FS, gen.C_SOUND, 3, 64, delay_interp=1)
+    assert np.all(plan.delay_fraction() == 0)
+    r = plan.beamform(torch.from_numpy(x[None]).cuda(), dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
+    ref = np.array([O.brute_force_esp(list(O.signed_root(x[:, t].astype(np.float64), 3)), 3) for t in range(64)])
+    assert np.max(np.abs(r - ref)) <= 1e-5 * np.max(np.abs(ref))
