@@ -99,16 +99,8 @@ struct dmas_plan_s {
   float* d_splane = nullptr;
   float* d_lp = nullptr;
   float* d_bp = nullptr;
-  float* d_scratch = nullptr;         // raw images of envelope-only kinds: 2 ping-pong halves
+  float* d_scratch = nullptr;         // raw images of envelope-only kinds
   size_t scratch_cap = 0;
-  // envelope of chunk c runs on env_stream while chunk c+1 beamforms on the caller's stream
-  // (k_beamform is FP32-ALU bound, the envelope HBM / tensor-core bound: they overlap)
-  // Off by default: measured on B200 the persistent tensor-core envelope CTA (one per SM, ~55k
-  // registers) cannot co-reside with beamform CTAs, so the kernels only time-share SMs (no gain).
-  bool overlap_env = false;
-  cudaStream_t env_stream = nullptr;
-  cudaEvent_t ev_bf[2] = {nullptr, nullptr}, ev_env[2] = {nullptr, nullptr};
-  bool env_used[2] = {false, false};  // ev_env[b] has been recorded (a previous call may still run)
   int64_t scratch_budget = 0;
 
   // host pipeline buffers (dmas_beamform_host)
@@ -169,11 +161,7 @@ void free_plan_memory(dmas_plan_s* p) {
   }
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
-  if (p->env_stream) cudaStreamDestroy(p->env_stream);
-  for (int b = 0; b < 2; ++b) {
-    if (p->ev_bf[b]) cudaEventDestroy(p->ev_bf[b]);
-    if (p->ev_env[b]) cudaEventDestroy(p->ev_env[b]);
-  }
+
   for (auto& r : p->recs) {
     cudaEventDestroy(r.ev0);
     cudaEventDestroy(r.ev1);
@@ -261,11 +249,8 @@ dmas_status validate(const dmas_plan_desc* d) {
 
 // Enqueue one chunk of frames: roots -> beamform -> envelopes.  `sig` / `outs_raw` / `outs_env`
 // already point at the chunk's first frame.
-// `pp` = ping-pong index of this chunk: its raw scratch half and its event pair.
 dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* const* raw_dst,
-                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st, int pp, bool wait_env) {
-  // the envelope that read this scratch half two chunks ago must be done before we overwrite it
-  if (wait_env) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[pp], 0));
+                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st) {
   if (p->mf_taps > 0) {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
       return dmas::launch_mf_roots(p->interp ? 1 : p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
@@ -293,11 +278,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.cf_eps = p->cf_eps;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
-  cudaStream_t es = p->overlap_env ? p->env_stream : st;
-  if (p->overlap_env) {
-    CUDA_TRY(cudaEventRecord(p->ev_bf[pp], st));
-    CUDA_TRY(cudaStreamWaitEvent(es, p->ev_bf[pp], 0));
-  }
+  cudaStream_t es = st;
   const int64_t rows = (int64_t)nf * p->n_dirs;
   for (int k = 0; k < dmas::N_KINDS; ++k) {
     if (!((env_kinds >> k) & 1u)) continue;
@@ -316,10 +297,6 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
                                              p->bp_taps, es);
       }));
     }
-  }
-  if (p->overlap_env) {
-    CUDA_TRY(cudaEventRecord(p->ev_env[pp], es));
-    p->env_used[pp] = true;
   }
   return DMAS_OK;
 }
@@ -353,21 +330,12 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
   const int n_scratch = popcount5(env_only);
   const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
   int32_t chunk = std::min(p->chunk_cap, n_frames);
-  const int halves = p->overlap_env ? 2 : 1;
-  if (env_k && p->overlap_env) {
-    if (!p->env_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->env_stream, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-      if (!p->ev_bf[b]) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_bf[b], cudaEventDisableTiming));
-      if (!p->ev_env[b]) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_env[b], cudaEventDisableTiming));
-    }
-  }
   if (n_scratch > 0) {
-    const int64_t fit = p->scratch_budget / (int64_t)(halves * frame_img * n_scratch);   // ping-pong halves
+    const int64_t fit = p->scratch_budget / (int64_t)(frame_img * n_scratch);
     chunk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(chunk, fit));
-    const size_t need = halves * (size_t)chunk * n_scratch * frame_img;
+    const size_t need = (size_t)chunk * n_scratch * frame_img;
     if (need > p->scratch_cap) {
       CUDA_TRY(cudaStreamSynchronize(st));
-      if (p->env_stream) CUDA_TRY(cudaStreamSynchronize(p->env_stream));
       cudaFree(p->d_scratch);
       p->d_scratch = nullptr;
       p->scratch_cap = 0;
@@ -375,29 +343,19 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
       p->scratch_cap = need;
     }
   }
-  // scratch halves may still be read by envelopes of a previous call on another stream
-  for (int b = 0; b < 2; ++b)
-    if (p->env_used[b]) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[b], 0));
-  int c = 0;
-  for (int32_t f0 = 0; f0 < n_frames; f0 += chunk, ++c) {
+  for (int32_t f0 = 0; f0 < n_frames; f0 += chunk) {
     const int32_t nf = std::min(chunk, n_frames - f0);
-    const int pp = p->overlap_env ? (c & 1) : 0;
-    float* scratch_half = p->d_scratch ? p->d_scratch + (size_t)pp * chunk * n_scratch * p->n_dirs * p->T : nullptr;
     float* raw_dst[dmas::N_KINDS] = {};
     float* env_dst[dmas::N_KINDS] = {};
     int s = 0;
     for (int k = 0; k < dmas::N_KINDS; ++k) {
       if ((raw_k >> k) & 1u) raw_dst[k] = const_cast<float*>(raw_user[k]) + (size_t)f0 * p->n_dirs * p->T;
-      else if ((env_only >> k) & 1u) raw_dst[k] = scratch_half + (size_t)(s++) * chunk * p->n_dirs * p->T;
+      else if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
       if ((env_k >> k) & 1u) env_dst[k] = env_user[k] + (size_t)f0 * p->n_dirs * p->T_out;
     }
     const float* sig = signals + (size_t)f0 * p->n_mics * p->T_in;
-    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, pp, p->overlap_env && env_k && c >= 2);
+    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st);
     if (rc != DMAS_OK) return rc;
-  }
-  if (env_k && p->overlap_env) {                 // the caller's stream sees every envelope
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[(c - 1) & 1], 0));
-    if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_env[c & 1], 0));
   }
   return DMAS_OK;
 }

@@ -459,3 +459,32 @@ def test_linear_presteer_with_matched_filter_and_slices(dm):
     r = plan.beamform(torch.from_numpy(x[None]).cuda(), dm.RAW(dm.KIND_DMAS))[("raw", "dmas")].cpu().numpy()[0, 0]
     ref = np.array([O.brute_force_esp(list(O.signed_root(x[:, t].astype(np.float64), 3)), 3) for t in range(64)])
     assert np.max(np.abs(r - ref)) <= 1e-5 * np.max(np.abs(ref))
+
+
+def test_sharded_beamformer_nccl_single_rank(dm):
+    """parallel.ShardedBeamformer through a real NCCL process group (world size 1 here; the
+    multi-rank host logic is covered with gloo in tests/test_parallel.py): broadcast + beamform +
+    gather reproduce the plain plan bitwise."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2511_09165_b200 import parallel
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        cfg = gen.config("C2")
+        x = torch.from_numpy(cfg["signals"]).cuda()
+        what = dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS)
+        sb = parallel.ShardedBeamformer(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"])
+        got = sb.beamform(x, what, src=0, gather_to=0)
+        ref = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"]).beamform(x, what)
+        torch.cuda.synchronize()
+        for k in ref:
+            assert torch.equal(got[k], ref[k]), k
+        sb.close()
+    finally:
+        dist.destroy_process_group()
