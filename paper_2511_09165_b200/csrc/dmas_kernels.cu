@@ -386,10 +386,60 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+// Accumulate microphones [i0, i1) of one direction into the thread's 8 pixels.  `wl` = window +
+// lane, `oq` = the direction's word offsets, `aq` its fractions (INTERP: the window holds m and
+// x = m[j] + alpha (m[j + 1] - m[j]), roots on the fly on the SFU; NEXT-2).
+template <int P, bool INTERP>
+__device__ __forceinline__ void bf_accumulate(Acc<P> (&acc)[BF_KT], const float* wl, const int32_t* oq,
+                                              const float* aq, int i0, int i1) {
+  if (INTERP) {
+#pragma unroll BF_UNROLL
+    for (int i = i0; i < i1; ++i) {
+      const float* w = wl + oq[i];
+      const float al = aq[i];
+#pragma unroll
+      for (int k = 0; k < BF_KT; ++k) {
+        const float m0 = w[32 * k], m1 = w[32 * k + 1];
+        acc_add<P>(acc[k], root_fast<P>(fmaf(al, m1 - m0, m0)));
+      }
+    }
+  } else {
+#pragma unroll BF_UNROLL
+    for (int i = i0; i < i1; ++i) {
+      const float* w = wl + oq[i];
+#pragma unroll
+      for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
+    }
+  }
+}
+
+// Newton-Girard + CF epilogue and coalesced stores of one direction's 8 pixels.
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
-// INTERP (NEXT-2): the window holds m (not roots); per (psi, mic) a fraction alpha in [0, 1):
-// x = m[j] + alpha (m[j + 1] - m[j]), roots on the fly on the SFU.
+template <int P, int KM>
+__device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> (&acc)[BF_KT], int64_t f, int64_t psi,
+                                            int64_t t0, int lane) {
+  const bool full_t = t0 + BF_T <= a.T;
+  const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
+#pragma unroll
+  for (int k = 0; k < BF_KT; ++k) {
+    if (!full_t && t0 + lane + 32 * k >= a.T) continue;
+    float A, B, E;
+    acc_final<P>(acc[k], A, B, E);
+    const float cf = A * A * rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps));
+    if (KM == 4) {
+      a.out[2][o + 32 * k] = E * cf;
+    } else {
+      if (a.out[0]) a.out[0][o + 32 * k] = A;
+      if (a.out[1]) a.out[1][o + 32 * k] = E;
+      if (a.out[2]) a.out[2][o + 32 * k] = E * cf;
+      if (a.out[3]) a.out[3][o + 32 * k] = A * cf;
+      if (a.out[4]) a.out[4][o + 32 * k] = cf;
+    }
+  }
+}
+
+// Main kernel: the whole array's window staged once per CTA and reused by BF_PSI directions.
 template <int P, int KM, bool INTERP>
 __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
@@ -428,68 +478,97 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   __syncthreads();
   mbar_wait(&bar, 0);
 
-  const float* wl = win + lane;
-  const bool full_t = t0 + BF_T <= a.T;
   for (int q = warp; q < npsi; q += BF_WARPS) {
     Acc<P> acc[BF_KT];
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
-    const int32_t* oq = offs + q * n_mics;
-    if (INTERP) {
-      const float* aq = alph + q * n_mics;
-#pragma unroll BF_UNROLL
-      for (int i = 0; i < n_mics; ++i) {
-        const float* w = wl + oq[i];
-        const float al = aq[i];
-#pragma unroll
-        for (int k = 0; k < BF_KT; ++k) {
-          const float m0 = w[32 * k], m1 = w[32 * k + 1];
-          acc_add<P>(acc[k], root_fast<P>(fmaf(al, m1 - m0, m0)));
-        }
-      }
-    } else {
-#pragma unroll BF_UNROLL
-      for (int i = 0; i < n_mics; ++i) {
-        const float* w = wl + oq[i];
-#pragma unroll
-        for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], w[32 * k]);
-      }
-    }
-    const int64_t o = (f * a.n_dirs + psi0 + q) * a.T + t0 + lane;
-#pragma unroll
-    for (int k = 0; k < BF_KT; ++k) {
-      if (!full_t && t0 + lane + 32 * k >= a.T) continue;
-      float A, B, E;
-      acc_final<P>(acc[k], A, B, E);
-      const float cf = A * A * rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps));
-      if (KM == 4) {
-        a.out[2][o + 32 * k] = E * cf;
-      } else {
-        if (a.out[0]) a.out[0][o + 32 * k] = A;
-        if (a.out[1]) a.out[1][o + 32 * k] = E;
-        if (a.out[2]) a.out[2][o + 32 * k] = E * cf;
-        if (a.out[3]) a.out[3][o + 32 * k] = A * cf;
-        if (a.out[4]) a.out[4][o + 32 * k] = cf;
-      }
-    }
+    bf_accumulate<P, INTERP>(acc, win + lane, offs + q * n_mics, alph + q * n_mics, 0, n_mics);
+    bf_epilogue<P, KM>(a, acc, f, psi0 + q, t0, lane);
   }
 }
 
-size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp) {
+// Large arrays (the whole window would not fit in shared memory, e.g. the 500-mic hexagonal
+// arrays of PAPER.md:243-247): CTA = BF_PSI_MG directions (one per warp) x BF_T samples; the
+// microphones stream through two TMA-filled window buffers of a.mg rows each (group g + 1 loads
+// while group g accumulates).  Same per-pixel arithmetic, microphone order and epilogue.
+template <int P, int KM, bool INTERP>
+__global__ void __launch_bounds__(BF_THREADS, 2) k_beamform_mg(const BeamformArgs a) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int32_t n_mics = a.n_mics, W = a.W, MG = a.mg;
+  float* win = smem;                                   // [2][MG][W]
+  int32_t* offs = reinterpret_cast<int32_t*>(smem + (size_t)2 * MG * W);  // [BF_PSI_MG][n_mics]
+  float* alph = reinterpret_cast<float*>(offs + BF_PSI_MG * n_mics);      // [BF_PSI_MG][n_mics] (INTERP)
+
+  const int64_t t0 = (int64_t)blockIdx.x * BF_T;
+  const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI_MG;
+  const int64_t f = blockIdx.z;
+  const int npsi = (int)min((int64_t)BF_PSI_MG, a.n_dirs - psi0);
+  const int32_t lo = __ldg(a.tile_lo + blockIdx.y);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_groups = (n_mics + MG - 1) / MG;
+  const float* src = a.splane + (f * n_mics) * a.Tp + a.G + t0 + lo;
+
+  auto issue = [&](int g) {                            // thread 0: TMA one microphone group
+    const int i0 = g * MG, i1 = min(n_mics, i0 + MG);
+    const uint32_t row_bytes = (uint32_t)W * 4u;
+    float* dst = win + (size_t)(g & 1) * MG * W;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[g & 1], row_bytes * (uint32_t)(i1 - i0));
+    for (int i = i0; i < i1; ++i) bulk_g2s(dst + (size_t)(i - i0) * W, src + (int64_t)i * a.Tp, row_bytes, &bar[g & 1]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) issue(0);
+  for (int q = warp; q < npsi; q += BF_WARPS) {
+    const int32_t* drow = a.delays + (psi0 + q) * n_mics;
+    for (int i = lane; i < n_mics; i += 32) {
+      offs[q * n_mics + i] = (i % MG) * W + (__ldg(drow + i) - lo);     // offset inside the group buffer
+      if (INTERP) alph[q * n_mics + i] = __ldg(a.alpha + (psi0 + q) * n_mics + i);
+    }
+  }
+  __syncthreads();
+
+  const int q = warp;                                  // BF_PSI_MG == BF_WARPS: one direction per warp
+  Acc<P> acc[BF_KT];
+#pragma unroll
+  for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
+  for (int g = 0; g < n_groups; ++g) {
+    if (threadIdx.x == 0 && g + 1 < n_groups) issue(g + 1);   // its buffer was released by the last barrier
+    mbar_wait(&bar[g & 1], (uint32_t)((g >> 1) & 1));
+    if (q < npsi)
+      bf_accumulate<P, INTERP>(acc, win + (size_t)(g & 1) * MG * W + lane, offs + q * n_mics, alph + q * n_mics,
+                               g * MG, min(n_mics, (g + 1) * MG));
+    __syncthreads();
+  }
+  if (q < npsi) bf_epilogue<P, KM>(a, acc, f, psi0 + q, t0, lane);
+}
+
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
+  if (mg > 0) return (size_t)2 * mg * W * sizeof(float) + (size_t)BF_PSI_MG * n_mics * (interp ? 8 : 4);
   return (size_t)n_mics * W * sizeof(float) + (size_t)BF_PSI * n_mics * (interp ? 8 : 4);
 }
 
 template <int P>
 static cudaError_t configure_order(int bytes) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform<P, 31, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, true>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, true>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 4, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 31, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 4, true>, attr, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform_mg<P, 31, true>, attr, bytes);
 }
 
-cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp) {
-  const int bytes = (int)beamform_smem_bytes(n_mics, W, interp);
+cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
+  const int bytes = (int)beamform_smem_bytes(n_mics, W, interp, mg);
   cudaError_t e;
   if ((e = configure_order<2>(bytes))) return e;
   if ((e = configure_order<3>(bytes))) return e;
@@ -503,6 +582,16 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp) {
 template <int P>
 static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
+  if (a.mg > 0) {
+    if (a.alpha) {
+      if (only_cfdmas) k_beamform_mg<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_mg<P, 31, true><<<grid, BF_THREADS, smem, st>>>(a);
+    } else {
+      if (only_cfdmas) k_beamform_mg<P, 4, false><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_mg<P, 31, false><<<grid, BF_THREADS, smem, st>>>(a);
+    }
+    return;
+  }
   if (a.alpha) {
     if (only_cfdmas) k_beamform<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
     else k_beamform<P, 31, true><<<grid, BF_THREADS, smem, st>>>(a);
@@ -514,9 +603,10 @@ static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStre
 
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
   const int64_t ntt = (a.T + BF_T - 1) / BF_T;
-  const int64_t npt = (a.n_dirs + BF_PSI - 1) / BF_PSI;
+  const int psi_tile = a.mg > 0 ? BF_PSI_MG : BF_PSI;
+  const int64_t npt = (a.n_dirs + psi_tile - 1) / psi_tile;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr);
+  const size_t smem = beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;
     case 3: launch_order<3>(a, grid, smem, st); break;

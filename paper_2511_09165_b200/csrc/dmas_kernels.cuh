@@ -26,6 +26,7 @@ constexpr int BF_KT = DMAS_BF_KT;
 constexpr int BF_T = 32 * BF_KT;
 constexpr int BF_PSI = DMAS_BF_PSI;
 constexpr int BF_UNROLL = DMAS_BF_UNROLL;
+constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per warp
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
 constexpr int ENV_THREADS = 256;
@@ -47,6 +48,7 @@ struct BeamformArgs {
   const int32_t* tile_lo;   // [n_psi_tiles] window origin (relative to t0) of each psi tile, %4 == 0
   float* out[N_KINDS];      // raw-image destinations [frames][n_dirs][T] (nullptr = kind not written)
   const float* alpha;       // [n_dirs][n_mics] fractional delays in [0, 1) (linear pre-steering), or null
+  int32_t mg;               // > 0: large-array path, microphones staged in groups of mg (tiles of BF_PSI_MG)
   int64_t Tp, G, T, n_dirs;
   int32_t n_mics, W;        // W = staged samples per mic row (multiple of 4)
   float n_mics_f, cf_eps;
@@ -73,8 +75,8 @@ cudaError_t mf_configure(int32_t Lp);
 
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
-size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp);
-cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp);   // opt-in to > 48 KB dynamic smem
+size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg);
+cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg);   // > 48 KB dynamic smem
 
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).
 cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,

@@ -94,6 +94,7 @@ struct dmas_plan_s {
   int32_t* d_delays = nullptr;
   int32_t* d_tile_lo = nullptr;
   int32_t W = 0;                      // staged window per mic (beamform)
+  int32_t mg = 0;                     // > 0: large-array path, microphones per staged group
   int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
   int32_t chunk_cap = 1;              // frames the signed-root plane holds
   float* d_splane = nullptr;
@@ -195,7 +196,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (!d->dir_az_el) return fail(DMAS_ERR_NULL, "dir_az_el is NULL");
   if (d->n_mics < 1) return fail(DMAS_ERR_INVALID, "n_mics < 1");
   if (d->n_dirs < 1) return fail(DMAS_ERR_INVALID, "n_dirs < 1");
-  if (d->n_dirs > (int64_t)65535 * dmas::BF_PSI) return fail(DMAS_ERR_INVALID, "n_dirs too large");
+  if (d->n_dirs > (int64_t)65535 * dmas::BF_PSI_MG) return fail(DMAS_ERR_INVALID, "n_dirs too large");
   if (d->n_samples < 1) return fail(DMAS_ERR_INVALID, "n_samples < 1");
   if (d->n_samples > ((int64_t)1 << 30)) return fail(DMAS_ERR_INVALID, "n_samples too large");
   if (!(d->fs_hz > 0) || !std::isfinite(d->fs_hz)) return fail(DMAS_ERR_INVALID, "fs_hz must be > 0");
@@ -267,6 +268,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.delays = p->d_delays;
   a.tile_lo = p->d_tile_lo;
   a.alpha = p->interp ? p->d_alpha : nullptr;
+  a.mg = p->mg;
   for (int k = 0; k < dmas::N_KINDS; ++k) a.out[k] = raw_dst[k];
   a.Tp = p->Tp;
   a.G = p->G;
@@ -464,37 +466,54 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   cudaFree(d_u);
   cudaFree(d_pos);
 
-  // ---- beamform staging metadata: per psi tile window origin (aligned down to 4) and width
-  const int64_t n_pt = (nd + dmas::BF_PSI - 1) / dmas::BF_PSI;
-  std::vector<int32_t> tile_lo((size_t)n_pt);
-  p->dmin = INT32_MAX;
-  p->dmax = INT32_MIN;
-  int32_t wmax = 0, lo_min = INT32_MAX, lo_max = INT32_MIN;
-  for (int64_t t = 0; t < n_pt; ++t) {
-    int32_t lo = INT32_MAX, hi = INT32_MIN;
-    const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BF_PSI);
-    for (int64_t a = t * dmas::BF_PSI; a < a1; ++a)
-      for (int i = 0; i < nm; ++i) {
-        const int32_t v = p->h_delays[(size_t)a * nm + i];
-        lo = std::min(lo, v);
-        hi = std::max(hi, v);
-      }
-    p->dmin = std::min(p->dmin, lo);
-    p->dmax = std::max(p->dmax, hi);
-    const int32_t lo_al = (int32_t)(std::floor(lo / 4.0) * 4);
-    tile_lo[(size_t)t] = lo_al;
-    lo_min = std::min(lo_min, lo_al);
-    lo_max = std::max(lo_max, lo_al);
-    wmax = std::max(wmax, dmas::BF_T + (hi - lo_al) + (p->interp ? 1 : 0));   // + m[j + 1] when interpolating
+  // ---- beamform staging metadata: per psi tile window origin (aligned down to 4) and width.
+  // Classic path (whole-array window, BF_PSI directions per CTA) when it fits in <= 116 KB of
+  // shared memory (2+ CTAs/SM); otherwise the large-array path streams microphone groups.
+  int32_t lo_min = INT32_MAX, lo_max = INT32_MIN;
+  std::vector<int32_t> tile_lo;
+  auto make_tiles = [&](int psi_tile) {
+    const int64_t n_pt = (nd + psi_tile - 1) / psi_tile;
+    tile_lo.assign((size_t)n_pt, 0);
+    p->dmin = INT32_MAX;
+    p->dmax = INT32_MIN;
+    lo_min = INT32_MAX;
+    lo_max = INT32_MIN;
+    int32_t wmax = 0;
+    for (int64_t t = 0; t < n_pt; ++t) {
+      int32_t lo = INT32_MAX, hi = INT32_MIN;
+      const int64_t a1 = std::min<int64_t>(nd, (t + 1) * psi_tile);
+      for (int64_t a = t * psi_tile; a < a1; ++a)
+        for (int i = 0; i < nm; ++i) {
+          const int32_t v = p->h_delays[(size_t)a * nm + i];
+          lo = std::min(lo, v);
+          hi = std::max(hi, v);
+        }
+      p->dmin = std::min(p->dmin, lo);
+      p->dmax = std::max(p->dmax, hi);
+      const int32_t lo_al = (int32_t)(std::floor(lo / 4.0) * 4);
+      tile_lo[(size_t)t] = lo_al;
+      lo_min = std::min(lo_min, lo_al);
+      lo_max = std::max(lo_max, lo_al);
+      wmax = std::max(wmax, dmas::BF_T + (hi - lo_al) + (p->interp ? 1 : 0));   // + m[j + 1] when interpolating
+    }
+    p->W = (wmax + 3) / 4 * 4;
+  };
+  make_tiles(dmas::BF_PSI);
+  p->mg = 0;
+  if (dmas::beamform_smem_bytes(nm, p->W, p->interp, 0) > (size_t)116 * 1024) {
+    make_tiles(dmas::BF_PSI_MG);
+    const int64_t fixed = (int64_t)dmas::BF_PSI_MG * nm * (p->interp ? 8 : 4);
+    int64_t mg = ((int64_t)100 * 1024 - fixed) / (8 * (int64_t)p->W);
+    mg = std::max<int64_t>(4, std::min<int64_t>(mg / 4 * 4, nm));
+    p->mg = (int32_t)mg;
   }
-  p->W = (wmax + 3) / 4 * 4;
-  const size_t smem = dmas::beamform_smem_bytes(nm, p->W, p->interp);
+  const size_t smem = dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (smem + 64 > (size_t)smem_optin)
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
-  PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp));
+  PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp, p->mg));
   PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
   PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
 
@@ -681,7 +700,7 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->device = p->device;
   info->d_min = p->dmin;
   info->d_max = p->dmax;
-  info->psi_tile = dmas::BF_PSI;
+  info->psi_tile = p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
   info->t_tile = dmas::BF_T;
   info->window = p->W;
   info->chunk_frames = p->chunk_cap;

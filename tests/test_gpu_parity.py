@@ -488,3 +488,34 @@ def test_sharded_beamformer_nccl_single_rank(dm):
         sb.close()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ large arrays (microphone-group path)
+@pytest.mark.parametrize("kind", ["disk160", "hex3cm", "hex6cm"])
+def test_large_array_parity(dm, kind):
+    """Arrays too large for one shared-memory window (e.g. the 5 mm hexagonal lattices of
+    PAPER.md:243-247) stream microphone groups through the TMA window; same arithmetic."""
+    if kind == "disk160":
+        mic, p, T = gen.disk_array(160, 0.10, 3.5e-3, seed=12), 2, 700
+    elif kind == "hex3cm":
+        mic, p, T = gen.hex_array(0.03), 3, 512
+    else:
+        mic, p, T = gen.hex_array(0.06), 2, 512
+    dirs = gen.az_el_grid(9, 80.0, 2, 10.0)
+    sig = gen.random_signals(2, len(mic), T, seed=len(mic), sparsity=0.1)
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, p, sig, what_all(dm))
+    assert plan.info["psi_tile"] == 8            # the microphone-group path was taken
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
+    for key in ref:
+        assert_parity(g[key], ref[key], f"{kind} {key}")
+    # and with linear pre-steering
+    plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, p, sig[:1], dm.RAW(dm.KIND_CFDMAS), delay_interp=1)
+    d0, al = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, mode="linear")
+    assert_parity(g[("raw", "cfdmas")], O.beamform_frame(sig[0], d0, p, alpha=al)["cfdmas"][None], f"{kind} linear")
+
+
+def test_classic_path_for_benchmark_configs(dm):
+    for name in ("C4", "C5"):
+        cfg = gen.config(name, frames=1)
+        plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"])
+        assert plan.info["psi_tile"] == 32, (name, plan.info)

@@ -436,3 +436,17 @@ def test_linear_presteer_aligns_physical_plane_wave():
     cf_near = O.beamform_frame(m, d, 2)["cf"][0, 1300:1325].max()
     cf_lin = O.beamform_frame(m, d0, 2, alpha=al)["cf"][0, 1300:1325].max()
     assert cf_lin > cf_near > 0.5
+
+
+def test_hex_lattice_counts():
+    """5 mm hexagonal lattice, radius 1 cm -> 19 microphones (paper's lower
+    bound); radius 2.4 mm -> 1.  At 6 cm a site-centred lattice gives 517, not the
+    paper's "513" (513 = 3 mod 6 cannot come from a 6-fold-symmetric
+    site-centred lattice) — recorded, not matched."""
+    assert len(gen.hex_array(0.0024)) == 1
+    assert len(gen.hex_array(0.01)) == 19
+    assert len(gen.hex_array(0.06)) == 517
+    a = gen.hex_array(0.03)
+    assert np.allclose(a[:, 0], 0) and np.allclose(a.mean(axis=0), 0, atol=1e-12)
+    dist = np.linalg.norm(a[:, None, 1:] - a[None, :, 1:], axis=-1) + np.eye(len(a))
+    assert np.isclose(dist.min(), 5e-3)

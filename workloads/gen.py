@@ -50,6 +50,21 @@ def disk_array(n: int, diameter: float = 0.10, min_spacing: float = 6e-3, seed: 
     return np.stack([np.zeros(n), yz[:, 0], yz[:, 1]], axis=1)
 
 
+def hex_array(radius: float, edge: float = 5e-3):
+    """Microphones on a hexagonal (triangular) lattice of edge `edge`, one at the origin, all
+    lattice points with |p| <= radius, in the y-z plane (Fig. 6: 5 mm edge,
+    radius 1..6 cm, "19--513 microphones")."""
+    n = int(radius / edge) + 2
+    pts = []
+    for j in range(-2 * n, 2 * n + 1):
+        for i in range(-2 * n, 2 * n + 1):
+            y = edge * (i + 0.5 * j)
+            z = edge * (math.sqrt(3.0) / 2.0) * j
+            if y * y + z * z <= radius * radius * (1 + 1e-12):
+                pts.append((0.0, y, z))
+    return np.array(sorted(pts, key=lambda q: (q[2], q[1])))
+
+
 # ------------------------------------------------------------------ grids
 def az_grid_deg(az_deg, el_deg: float = 0.0):
     az = np.deg2rad(np.asarray(az_deg, dtype=np.float64))
