@@ -25,7 +25,8 @@ constexpr int BF_WARPS = BF_THREADS / 32;
 constexpr int BF_KT = DMAS_BF_KT;
 constexpr int BF_T = 32 * BF_KT;
 constexpr int BF_PSI = DMAS_BF_PSI;
-constexpr int BF_UNROLL = DMAS_BF_UNROLL;
+constexpr int BF_UNROLL = DMAS_BF_UNROLL;   // interpolating / large-array paths
+constexpr int BF_MIC_PAD = 8;              // classic path: offset rows padded to 8 microphones
 constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per warp
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
