@@ -353,6 +353,17 @@ template <> __device__ __forceinline__ void acc_final<5>(const Acc<5>& c, float&
        30.f * P1 * P4 + 24.f * P5) * (1.f / 120.f);
 }
 
+// E for the streaming CF-DMAS epilogue: p = 2 returns 2 E_2 (its 1/2 is folded into the CF
+// reciprocal there); other orders return E_p.
+template <int P> __device__ __forceinline__ void acc_final_cfdmas(const Acc<P>& c, float& A, float& B, float& E) {
+  acc_final<P>(c, A, B, E);
+}
+template <> __device__ __forceinline__ void acc_final_cfdmas<2>(const Acc<2>& c, float& A, float& B, float& E) {
+  A = c.pa.y;
+  B = c.pb.y;
+  E = c.pa.x * c.pa.x - c.pb.x;
+}
+
 // Signed root of an interpolated sample, on the fly (SFU approximations, rel. error ~2^-22).
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -456,6 +467,20 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
                                             int64_t t0, int lane) {
   const bool full_t = t0 + BF_T <= a.T;
   const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
+  if (KM == 4 && full_t) {
+    // streaming CF-DMAS request, whole tile in range: no per-pixel guards; for p = 2 the 1/2 of
+    // E_2 moves into the reciprocal, rcp(2(N B + eps)) = rcp(N B + eps)/2 exactly (power-of-two
+    // scaling), so the value is bit-identical to the generic epilogue's.
+    float* dst = a.out[2] + o;
+    const float n2 = (P == 2 ? 2.f : 1.f) * a.n_mics_f, e2 = (P == 2 ? 2.f : 1.f) * a.cf_eps;
+#pragma unroll
+    for (int k = 0; k < BF_KT; ++k) {
+      float A, B, E;
+      acc_final_cfdmas<P>(acc[k], A, B, E);
+      dst[32 * k] = E * (A * A * rcp_approx(fmaf(n2, B, e2)));
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < BF_KT; ++k) {
     if (!full_t && t0 + lane + 32 * k >= a.T) continue;
@@ -500,17 +525,21 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t row_bytes = (uint32_t)W * 4u;
-    mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics);
+    const uint32_t offs_bytes = INTERP ? 0u : (uint32_t)(BF_PSI * n_pad) * 4u;
+    mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes);
+    if (!INTERP) bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);   // plan-built
     const float* src = a.splane + (f * n_mics) * a.Tp + a.G + t0 + lo;
     for (int i = 0; i < n_mics; ++i) bulk_g2s(win + (size_t)i * W, src + (int64_t)i * a.Tp, row_bytes, &bar);
   }
-  // delay rows of this psi tile -> smem word offsets into the window (overlaps the TMA)
   for (int j = threadIdx.x; j < BF_T; j += BF_THREADS) zero[j] = 0.f;
-  for (int q = warp; q < npsi; q += BF_WARPS) {
-    const int32_t* drow = a.delays + (psi0 + q) * n_mics;
-    for (int i = lane; i < n_pad; i += 32) {
-      offs[q * n_pad + i] = i < n_mics ? i * W + (__ldg(drow + i) - lo) : n_mics * W;
-      if (INTERP) alph[q * n_mics + i] = __ldg(a.alpha + (psi0 + q) * n_mics + i);
+  if (INTERP) {
+    // delay rows of this psi tile -> smem word offsets + fractions (overlaps the TMA)
+    for (int q = warp; q < npsi; q += BF_WARPS) {
+      const int32_t* drow = a.delays + (psi0 + q) * n_mics;
+      for (int i = lane; i < n_mics; i += 32) {
+        offs[q * n_pad + i] = i * W + (__ldg(drow + i) - lo);
+        alph[q * n_mics + i] = __ldg(a.alpha + (psi0 + q) * n_mics + i);
+      }
     }
   }
   __syncthreads();

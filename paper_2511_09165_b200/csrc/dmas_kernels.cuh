@@ -47,6 +47,8 @@ struct BeamformArgs {
   const float* splane;      // [frames][n_mics][Tp]; sample t of (f, i) at column G + t; zero guards
   const int32_t* delays;    // [n_dirs][n_mics] int32 sample delays d[psi][i]
   const int32_t* tile_lo;   // [n_psi_tiles] window origin (relative to t0) of each psi tile, %4 == 0
+  const int32_t* offs;      // classic integer path: [n_psi_tiles][BF_PSI][n_pad] window word offsets
+                            // i W + d - lo (padding microphones -> the zero block), built at plan time
   float* out[N_KINDS];      // raw-image destinations [frames][n_dirs][T] (nullptr = kind not written)
   const float* alpha;       // [n_dirs][n_mics] fractional delays in [0, 1) (linear pre-steering), or null
   int32_t mg;               // > 0: large-array path, microphones staged in groups of mg (tiles of BF_PSI_MG)
