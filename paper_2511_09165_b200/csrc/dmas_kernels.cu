@@ -275,6 +275,34 @@ template <> __device__ __forceinline__ void acc_add<5>(Acc<5>& c, float s) {
   c.b = fmaf(x, x, c.b);
 }
 
+// Interpolating path (NEXT-2): the interpolated sample v is x itself, so A and B take v directly
+// and only the powers of s = root(v) are formed (one FMUL fewer per microphone sample at p = 2).
+template <int P> __device__ __forceinline__ void acc_add_x(Acc<P>& c, float s, float x) { acc_add<P>(c, s); }
+template <> __device__ __forceinline__ void acc_add_x<2>(Acc<2>& c, float s, float x) {
+  const float2 sx = make_float2(s, x);
+  c.pa = __fadd2_rn(c.pa, sx);                      // P1 += s, A += x
+  c.pb = __ffma2_rn(sx, sx, c.pb);                  // P2 += s^2 (= |x|), B += x^2
+}
+template <> __device__ __forceinline__ void acc_add_x<3>(Acc<3>& c, float s, float x) {
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s * s));
+  c.a += x;                                          // = P3
+  c.b = fmaf(x, x, c.b);
+}
+template <> __device__ __forceinline__ void acc_add_x<4>(Acc<4>& c, float s, float x) {
+  const float s2 = s * s;
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
+  c.p34 = __fadd2_rn(c.p34, make_float2(s2 * s, fabsf(x)));   // P4 = sum |x|
+  c.a += x;
+  c.b = fmaf(x, x, c.b);
+}
+template <> __device__ __forceinline__ void acc_add_x<5>(Acc<5>& c, float s, float x) {
+  const float s2 = s * s;
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
+  c.p34 = __fadd2_rn(c.p34, make_float2(s2 * s, s2 * s2));
+  c.a += x;                                          // = P5
+  c.b = fmaf(x, x, c.b);
+}
+
 // Newton-Girard explicit expansions, exactly as printed.
 // General Newton-Girard formula (Eq. PAPER.md:136): E_n = sum over partitions (k_1..k_n) of n with
 // sum_i i k_i = n of (-1)^(n - sum k_i) prod_i P_i^{k_i} / (k_i! i^{k_i}); the partition list and
@@ -417,7 +445,8 @@ __device__ __forceinline__ void bf_accumulate(Acc<P> (&acc)[BF_KT], const float*
 #pragma unroll
       for (int k = 0; k < BF_KT; ++k) {
         const float m0 = w[32 * k], m1 = w[32 * k + 1];
-        acc_add<P>(acc[k], root_fast<P>(fmaf(al, m1 - m0, m0)));
+        const float v = fmaf(al, m1 - m0, m0);
+        acc_add_x<P>(acc[k], root_fast<P>(v), v);
       }
     }
   } else {
@@ -439,21 +468,36 @@ __device__ __forceinline__ void bf_accumulate(Acc<P> (&acc)[BF_KT], const float*
 // microphones per loop iteration: 8 for p <= 3 (measured +1.4% over 4 at p = 2), 4 above
 template <int P> __host__ __device__ constexpr int bf_unroll() { return P <= 3 ? 8 : 4; }
 static_assert(BF_MIC_PAD % 8 == 0, "offset rows are read as int4, up to 8 microphones per iteration");
-template <int P>
+template <int P, bool INTERP>
 __device__ __forceinline__ void bf_accumulate_padded(Acc<P> (&acc)[BF_KT], uint32_t la, const int32_t* oq,
-                                                     int n_pad) {
+                                                     const float* aq, int n_pad) {
   const int4* o4 = reinterpret_cast<const int4*>(oq);
+  const float4* a4 = reinterpret_cast<const float4*>(aq);
+  constexpr int U = INTERP ? 4 : bf_unroll<P>();
 #pragma unroll 1
-  for (int j = 0; j < n_pad / 4; j += bf_unroll<P>() / 4) {
+  for (int j = 0; j < n_pad / 4; j += U / 4) {
 #pragma unroll
-    for (int u = 0; u < bf_unroll<P>() / 4; ++u) {
+    for (int u = 0; u < U / 4; ++u) {
       const int4 o = o4[j + u];
       const int oo[4] = {o.x, o.y, o.z, o.w};
+      float aa[4] = {0.f, 0.f, 0.f, 0.f};
+      if (INTERP) {
+        const float4 al = a4[j + u];
+        aa[0] = al.x; aa[1] = al.y; aa[2] = al.z; aa[3] = al.w;
+      }
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const uint32_t addr = la + ((uint32_t)oo[h] << 2);
 #pragma unroll
-        for (int k = 0; k < BF_KT; ++k) acc_add<P>(acc[k], lds_f32(addr + 128u * k));
+        for (int k = 0; k < BF_KT; ++k) {
+          if (INTERP) {
+            const float m0 = lds_f32(addr + 128u * k), m1 = lds_f32(addr + 128u * k + 4u);
+            const float v = fmaf(aa[h], m1 - m0, m0);     // linear pre-steering (reading Q4b)
+            acc_add_x<P>(acc[k], root_fast<P>(v), v);
+          } else {
+            acc_add<P>(acc[k], lds_f32(addr + 128u * k));
+          }
+        }
       }
     }
   }
@@ -505,11 +549,11 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;
-  const int32_t n_pad = INTERP ? n_mics : (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
+  const int32_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
   float* win = smem;                                   // [n_mics][W]   staged S window
-  float* zero = smem + (size_t)n_mics * W;             // [BF_T] zeros (padding microphones)
-  int32_t* offs = reinterpret_cast<int32_t*>(zero + BF_T);               // [BF_PSI][n_pad]
-  float* alph = reinterpret_cast<float*>(offs + BF_PSI * n_pad);         // [BF_PSI][n_mics] (INTERP)
+  float* zero = smem + (size_t)n_mics * W;             // [BF_ZERO] zeros (padding microphones)
+  int32_t* offs = reinterpret_cast<int32_t*>(zero + BF_ZERO);            // [BF_PSI][n_pad]
+  float* alph = reinterpret_cast<float*>(offs + BF_PSI * n_pad);         // [BF_PSI][n_pad] (INTERP)
 
   const int64_t t0 = (int64_t)blockIdx.x * BF_T;
   const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
@@ -525,23 +569,14 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t row_bytes = (uint32_t)W * 4u;
-    const uint32_t offs_bytes = INTERP ? 0u : (uint32_t)(BF_PSI * n_pad) * 4u;
-    mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes);
-    if (!INTERP) bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);   // plan-built
+    const uint32_t offs_bytes = (uint32_t)(BF_PSI * n_pad) * 4u;
+    mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes * (INTERP ? 2u : 1u));
+    bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);       // plan-built
+    if (INTERP) bulk_g2s(alph, a.alpha_tab + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);
     const float* src = a.splane + (f * n_mics) * a.Tp + a.G + t0 + lo;
     for (int i = 0; i < n_mics; ++i) bulk_g2s(win + (size_t)i * W, src + (int64_t)i * a.Tp, row_bytes, &bar);
   }
-  for (int j = threadIdx.x; j < BF_T; j += BF_THREADS) zero[j] = 0.f;
-  if (INTERP) {
-    // delay rows of this psi tile -> smem word offsets + fractions (overlaps the TMA)
-    for (int q = warp; q < npsi; q += BF_WARPS) {
-      const int32_t* drow = a.delays + (psi0 + q) * n_mics;
-      for (int i = lane; i < n_mics; i += 32) {
-        offs[q * n_pad + i] = i * W + (__ldg(drow + i) - lo);
-        alph[q * n_mics + i] = __ldg(a.alpha + (psi0 + q) * n_mics + i);
-      }
-    }
-  }
+  for (int j = threadIdx.x; j < BF_ZERO; j += BF_THREADS) zero[j] = 0.f;
   __syncthreads();
   mbar_wait(&bar, 0);
 
@@ -549,10 +584,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     Acc<P> acc[BF_KT];
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) acc_zero<P>(acc[k]);
-    if (INTERP)
-      bf_accumulate<P, INTERP>(acc, win + lane, offs + q * n_pad, alph + q * n_mics, 0, n_mics);
-    else
-      bf_accumulate_padded<P>(acc, smem_u32(win + lane), offs + q * n_pad, n_pad);
+    bf_accumulate_padded<P, INTERP>(acc, smem_u32(win + lane), offs + q * n_pad, alph + q * n_pad, n_pad);
     bf_epilogue<P, KM>(a, acc, f, psi0 + q, t0, lane);
   }
 }
@@ -620,9 +652,8 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform_mg(const BeamformArg
 
 size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
   if (mg > 0) return (size_t)2 * mg * W * sizeof(float) + (size_t)BF_PSI_MG * n_mics * (interp ? 8 : 4);
-  const size_t n_pad = interp ? n_mics : (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
-  return ((size_t)n_mics * W + BF_T) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 +
-         (interp ? (size_t)BF_PSI * n_mics * 4 : 0);
+  const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
+  return ((size_t)n_mics * W + BF_ZERO) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
 template <int P>

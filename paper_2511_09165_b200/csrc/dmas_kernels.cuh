@@ -27,6 +27,7 @@ constexpr int BF_T = 32 * BF_KT;
 constexpr int BF_PSI = DMAS_BF_PSI;
 constexpr int BF_UNROLL = DMAS_BF_UNROLL;   // interpolating / large-array paths
 constexpr int BF_MIC_PAD = 8;              // classic path: offset rows padded to 8 microphones
+constexpr int BF_ZERO = 32 * 8 + 4;        // zero block for padding microphones (+1 sample read when interpolating)
 constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per warp
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
@@ -47,8 +48,9 @@ struct BeamformArgs {
   const float* splane;      // [frames][n_mics][Tp]; sample t of (f, i) at column G + t; zero guards
   const int32_t* delays;    // [n_dirs][n_mics] int32 sample delays d[psi][i]
   const int32_t* tile_lo;   // [n_psi_tiles] window origin (relative to t0) of each psi tile, %4 == 0
-  const int32_t* offs;      // classic integer path: [n_psi_tiles][BF_PSI][n_pad] window word offsets
-                            // i W + d - lo (padding microphones -> the zero block), built at plan time
+  const int32_t* offs;      // classic path: [n_psi_tiles][BF_PSI][n_pad] window word offsets i W + d - lo
+                            // (padding microphones -> the zero block), built at plan time
+  const float* alpha_tab;   // classic interpolating path: [n_psi_tiles][BF_PSI][n_pad] fractions (pad 0)
   float* out[N_KINDS];      // raw-image destinations [frames][n_dirs][T] (nullptr = kind not written)
   const float* alpha;       // [n_dirs][n_mics] fractional delays in [0, 1) (linear pre-steering), or null
   int32_t mg;               // > 0: large-array path, microphones staged in groups of mg (tiles of BF_PSI_MG)

@@ -93,7 +93,8 @@ struct dmas_plan_s {
   // device state
   int32_t* d_delays = nullptr;
   int32_t* d_tile_lo = nullptr;
-  int32_t* d_offs = nullptr;          // classic integer path: per-tile padded window offsets
+  int32_t* d_offs = nullptr;          // classic path: per-tile padded window offsets
+  float* d_alpha_tab = nullptr;       // classic interpolating path: per-tile padded fractions
   int32_t W = 0;                      // staged window per mic (beamform)
   int32_t mg = 0;                     // > 0: large-array path, microphones per staged group
   int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
@@ -152,6 +153,7 @@ void free_plan_memory(dmas_plan_s* p) {
   cudaFree(p->d_delays);
   cudaFree(p->d_tile_lo);
   cudaFree(p->d_offs);
+  cudaFree(p->d_alpha_tab);
   cudaFree(p->d_splane);
   cudaFree(p->d_lp);
   cudaFree(p->d_bp);
@@ -270,6 +272,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.delays = p->d_delays;
   a.tile_lo = p->d_tile_lo;
   a.offs = p->d_offs;
+  a.alpha_tab = p->d_alpha_tab;
   a.alpha = p->interp ? p->d_alpha : nullptr;
   a.mg = p->mg;
   for (int k = 0; k < dmas::N_KINDS; ++k) a.out[k] = raw_dst[k];
@@ -519,22 +522,32 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp, p->mg));
   PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
   PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  if (!p->interp && p->mg == 0) {
-    // classic integer path: every CTA of a psi tile (all t tiles, all frames) uses the same word
-    // offsets i W + d - lo into its staged window; build them once here, the kernel TMA-copies its
-    // tile's [BF_PSI][n_pad] block alongside the window.  Padding microphones (and directions past
-    // the grid end) point at the kernel's zero block at word n_mics W.
+  if (p->mg == 0) {
+    // classic path: every CTA of a psi tile (all t tiles, all frames) uses the same word offsets
+    // i W + d - lo into its staged window (and, interpolating, the same fractions); build them once
+    // here, the kernel TMA-copies its tile's [BF_PSI][n_pad] block(s) alongside the window.  Padding
+    // microphones (and directions past the grid end) point at the kernel's zero block at word
+    // n_mics W with fraction 0.
     const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
-    std::vector<int32_t> offs((size_t)tile_lo.size() * dmas::BF_PSI * n_pad, nm * p->W);
+    const size_t n_tab = tile_lo.size() * dmas::BF_PSI * n_pad;
+    std::vector<int32_t> offs(n_tab, nm * p->W);
+    std::vector<float> alph(p->interp ? n_tab : 0, 0.f);
     for (size_t t = 0; t < tile_lo.size(); ++t)
       for (int q = 0; q < dmas::BF_PSI; ++q) {
         const int64_t a = (int64_t)t * dmas::BF_PSI + q;
         if (a >= nd) break;
-        int32_t* row = offs.data() + ((size_t)t * dmas::BF_PSI + q) * n_pad;
-        for (int i = 0; i < nm; ++i) row[i] = i * p->W + (p->h_delays[(size_t)a * nm + i] - tile_lo[t]);
+        const size_t row = ((size_t)t * dmas::BF_PSI + q) * n_pad;
+        for (int i = 0; i < nm; ++i) {
+          offs[row + i] = i * p->W + (p->h_delays[(size_t)a * nm + i] - tile_lo[t]);
+          if (p->interp) alph[row + i] = p->h_alpha[(size_t)a * nm + i];
+        }
       }
-    PLAN_TRY(cudaMalloc(&p->d_offs, offs.size() * sizeof(int32_t)));
-    PLAN_TRY(cudaMemcpy(p->d_offs, offs.data(), offs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    PLAN_TRY(cudaMalloc(&p->d_offs, n_tab * sizeof(int32_t)));
+    PLAN_TRY(cudaMemcpy(p->d_offs, offs.data(), n_tab * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (p->interp) {
+      PLAN_TRY(cudaMalloc(&p->d_alpha_tab, n_tab * sizeof(float)));
+      PLAN_TRY(cudaMemcpy(p->d_alpha_tab, alph.data(), n_tab * sizeof(float), cudaMemcpyHostToDevice));
+    }
   }
 
   // ---- signed-root plane with zero guards: reads at t + d outside [0, T) return 0 (reading Q5)
