@@ -230,48 +230,50 @@ template <> __device__ __forceinline__ void acc_zero<4>(Acc<4>& c) { c.p12 = c.p
 template <> __device__ __forceinline__ void acc_zero<5>(Acc<5>& c) { c.p12 = c.p34 = make_float2(0.f, 0.f); c.a = c.b = 0.f; }
 
 // One microphone sample s = s_i(t, psi) of one pixel.  x = sgn(s)|s|^p is rebuilt from s
-// (exact up to rounding since s^p = sgn(x)^p |x| and the p = 2 / 4 cases take |s|).
+// (exact up to rounding since s^p = sgn(x)^p |x| and the p = 2 / 4 cases take |s|).  Explicit
+// IEEE intrinsics throughout (no contraction left to the compiler), so every kernel that
+// inlines these rounds identically.
 template <int P> __device__ __forceinline__ void acc_add(Acc<P>& c, float s) {
   float pw = s;                                          // s^k
-  c.pk[0] += s;
+  c.pk[0] = __fadd_rn(c.pk[0], s);
 #pragma unroll
   for (int k = 1; k < P; ++k) {
-    pw *= s;
-    c.pk[k] += pw;                                       // k = P - 1: s^P = x (odd P) or |x| (even P)
+    pw = __fmul_rn(pw, s);
+    c.pk[k] = __fadd_rn(c.pk[k], pw);                    // k = P - 1: s^P = x (odd P) or |x| (even P)
   }
   const float x = (P & 1) ? pw : copysignf(pw, s);
-  c.a += x;
+  c.a = __fadd_rn(c.a, x);
   c.b = fmaf(x, x, c.b);
 }
 template <> __device__ __forceinline__ void acc_add<2>(Acc<2>& c, float s) {
-  const float2 sx = make_float2(s, s * fabsf(s));   // (s, x)
+  const float2 sx = make_float2(s, __fmul_rn(s, fabsf(s)));   // (s, x)
   c.pa = __fadd2_rn(c.pa, sx);                      // P1 += s, A += x
   c.pb = __ffma2_rn(sx, sx, c.pb);                  // P2 += s^2 (= |x|), B += x^2
 }
 template <> __device__ __forceinline__ void acc_add<3>(Acc<3>& c, float s) {
-  const float s2 = s * s;
-  const float x = s2 * s;
+  const float s2 = __fmul_rn(s, s);
+  const float x = __fmul_rn(s2, s);
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
-  c.a += x;
+  c.a = __fadd_rn(c.a, x);
   c.b = fmaf(x, x, c.b);
 }
 template <> __device__ __forceinline__ void acc_add<4>(Acc<4>& c, float s) {
-  const float s2 = s * s;
-  const float s3 = s2 * s;
-  const float s4 = s2 * s2;                          // = |x|
+  const float s2 = __fmul_rn(s, s);
+  const float s3 = __fmul_rn(s2, s);
+  const float s4 = __fmul_rn(s2, s2);                // = |x|
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
   c.p34 = __fadd2_rn(c.p34, make_float2(s3, s4));
   c.a = fmaf(s3, fabsf(s), c.a);                     // x = sgn(s) s^4 (one FFMA, no LOP)
   c.b = fmaf(s4, s4, c.b);
 }
 template <> __device__ __forceinline__ void acc_add<5>(Acc<5>& c, float s) {
-  const float s2 = s * s;
-  const float s3 = s2 * s;
-  const float s4 = s2 * s2;
-  const float x = s4 * s;
+  const float s2 = __fmul_rn(s, s);
+  const float s3 = __fmul_rn(s2, s);
+  const float s4 = __fmul_rn(s2, s2);
+  const float x = __fmul_rn(s4, s);
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
   c.p34 = __fadd2_rn(c.p34, make_float2(s3, s4));
-  c.a += x;
+  c.a = __fadd_rn(c.a, x);
   c.b = fmaf(x, x, c.b);
 }
 
@@ -284,22 +286,22 @@ template <> __device__ __forceinline__ void acc_add_x<2>(Acc<2>& c, float s, flo
   c.pb = __ffma2_rn(sx, sx, c.pb);                  // P2 += s^2 (= |x|), B += x^2
 }
 template <> __device__ __forceinline__ void acc_add_x<3>(Acc<3>& c, float s, float x) {
-  c.p12 = __fadd2_rn(c.p12, make_float2(s, s * s));
-  c.a += x;                                          // = P3
+  c.p12 = __fadd2_rn(c.p12, make_float2(s, __fmul_rn(s, s)));
+  c.a = __fadd_rn(c.a, x);                           // = P3
   c.b = fmaf(x, x, c.b);
 }
 template <> __device__ __forceinline__ void acc_add_x<4>(Acc<4>& c, float s, float x) {
-  const float s2 = s * s;
+  const float s2 = __fmul_rn(s, s);
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
-  c.p34 = __fadd2_rn(c.p34, make_float2(s2 * s, fabsf(x)));   // P4 = sum |x|
-  c.a += x;
+  c.p34 = __fadd2_rn(c.p34, make_float2(__fmul_rn(s2, s), fabsf(x)));   // P4 = sum |x|
+  c.a = __fadd_rn(c.a, x);
   c.b = fmaf(x, x, c.b);
 }
 template <> __device__ __forceinline__ void acc_add_x<5>(Acc<5>& c, float s, float x) {
-  const float s2 = s * s;
+  const float s2 = __fmul_rn(s, s);
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
-  c.p34 = __fadd2_rn(c.p34, make_float2(s2 * s, s2 * s2));
-  c.a += x;                                          // = P5
+  c.p34 = __fadd2_rn(c.p34, make_float2(__fmul_rn(s2, s), __fmul_rn(s2, s2)));
+  c.a = __fadd_rn(c.a, x);                           // = P5
   c.b = fmaf(x, x, c.b);
 }
 
@@ -341,6 +343,11 @@ template <int N> struct PartitionTable {
     ks[i] = 0;
   }
 };
+// Every operation below is an explicit IEEE-rounded intrinsic (no FMA contraction left to the
+// compiler), so an expansion rounds identically in every kernel that inlines it.
+#define FM __fmul_rn
+#define FA __fadd_rn
+#define FS __fsub_rn
 template <int P> __device__ __forceinline__ void acc_final(const Acc<P>& c, float& A, float& B, float& E) {
   constexpr PartitionTable<P> tab{};
   A = c.a;
@@ -352,33 +359,47 @@ template <int P> __device__ __forceinline__ void acc_final(const Acc<P>& c, floa
 #pragma unroll
     for (int j = 0; j < P; ++j)
 #pragma unroll
-      for (int q = 0; q < tab.k[t][j]; ++q) term *= c.pk[j];
-    e += term;
+      for (int q = 0; q < tab.k[t][j]; ++q) term = FM(term, c.pk[j]);
+    e = FA(e, term);
   }
   E = e;
 }
 template <> __device__ __forceinline__ void acc_final<2>(const Acc<2>& c, float& A, float& B, float& E) {
   const float P1 = c.pa.x, P2 = c.pb.x;
   A = c.pa.y; B = c.pb.y;
-  E = 0.5f * (P1 * P1 - P2);
+  E = FM(0.5f, fmaf(P1, P1, -P2));                                  // (P1^2 - P2) / 2
 }
 template <> __device__ __forceinline__ void acc_final<3>(const Acc<3>& c, float& A, float& B, float& E) {
   const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.a;
   A = c.a; B = c.b;
-  E = (P1 * P1 * P1 + 2.f * P3 - 3.f * P1 * P2) * (1.f / 6.f);
+  // (P1^3 + 2 P3 - 3 P1 P2) / 6
+  const float t = FS(FA(FM(FM(P1, P1), P1), FM(2.f, P3)), FM(FM(3.f, P1), P2));
+  E = FM(t, 1.f / 6.f);
 }
 template <> __device__ __forceinline__ void acc_final<4>(const Acc<4>& c, float& A, float& B, float& E) {
   const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.p34.x, P4 = c.p34.y;
   A = c.a; B = c.b;
-  const float P1s = P1 * P1;
-  E = (P1s * P1s - 6.f * P4 + 3.f * P2 * P2 - 6.f * P2 * P1s + 8.f * P3 * P1) * (1.f / 24.f);
+  const float P1s = FM(P1, P1);
+  // (P1^4 - 6 P4 + 3 P2^2 - 6 P2 P1^2 + 8 P3 P1) / 24
+  float t = FS(FM(P1s, P1s), FM(6.f, P4));
+  t = FA(t, FM(FM(3.f, P2), P2));
+  t = FS(t, FM(FM(6.f, P2), P1s));
+  t = FA(t, FM(FM(8.f, P3), P1));
+  E = FM(t, 1.f / 24.f);
 }
 template <> __device__ __forceinline__ void acc_final<5>(const Acc<5>& c, float& A, float& B, float& E) {
   const float P1 = c.p12.x, P2 = c.p12.y, P3 = c.p34.x, P4 = c.p34.y, P5 = c.a;
   A = c.a; B = c.b;
-  const float P1s = P1 * P1;
-  E = (P1s * P1s * P1 - 10.f * P2 * P1s * P1 + 15.f * P2 * P2 * P1 + 20.f * P3 * P1s - 20.f * P3 * P2 -
-       30.f * P1 * P4 + 24.f * P5) * (1.f / 120.f);
+  const float P1s = FM(P1, P1);
+  // (P1^5 - 10 P2 P1^3 + 15 P2^2 P1 + 20 P3 P1^2 - 20 P3 P2 - 30 P1 P4 + 24 P5) / 120
+  float t = FM(FM(P1s, P1s), P1);
+  t = FS(t, FM(FM(FM(10.f, P2), P1s), P1));
+  t = FA(t, FM(FM(FM(15.f, P2), P2), P1));
+  t = FA(t, FM(FM(20.f, P3), P1s));
+  t = FS(t, FM(FM(20.f, P3), P2));
+  t = FS(t, FM(FM(30.f, P1), P4));
+  t = FA(t, FM(24.f, P5));
+  E = FM(t, 1.f / 120.f);
 }
 
 // E for the streaming CF-DMAS epilogue: p = 2 returns 2 E_2 (its 1/2 is folded into the CF
@@ -389,7 +410,7 @@ template <int P> __device__ __forceinline__ void acc_final_cfdmas(const Acc<P>& 
 template <> __device__ __forceinline__ void acc_final_cfdmas<2>(const Acc<2>& c, float& A, float& B, float& E) {
   A = c.pa.y;
   B = c.pb.y;
-  E = c.pa.x * c.pa.x - c.pb.x;
+  E = fmaf(c.pa.x, c.pa.x, -c.pb.x);
 }
 
 // Signed root of an interpolated sample, on the fly (SFU approximations, rel. error ~2^-22).
@@ -521,7 +542,7 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     for (int k = 0; k < BF_KT; ++k) {
       float A, B, E;
       acc_final_cfdmas<P>(acc[k], A, B, E);
-      dst[32 * k] = E * (A * A * rcp_approx(fmaf(n2, B, e2)));
+      dst[32 * k] = FM(E, FM(FM(A, A), rcp_approx(fmaf(n2, B, e2))));
     }
     return;
   }
@@ -530,14 +551,14 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     if (!full_t && t0 + lane + 32 * k >= a.T) continue;
     float A, B, E;
     acc_final<P>(acc[k], A, B, E);
-    const float cf = A * A * rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps));
+    const float cf = FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps)));
     if (KM == 4) {
-      a.out[2][o + 32 * k] = E * cf;
+      a.out[2][o + 32 * k] = FM(E, cf);
     } else {
       if (a.out[0]) a.out[0][o + 32 * k] = A;
       if (a.out[1]) a.out[1][o + 32 * k] = E;
-      if (a.out[2]) a.out[2][o + 32 * k] = E * cf;
-      if (a.out[3]) a.out[3][o + 32 * k] = A * cf;
+      if (a.out[2]) a.out[2][o + 32 * k] = FM(E, cf);
+      if (a.out[3]) a.out[3][o + 32 * k] = FM(A, cf);
       if (a.out[4]) a.out[4][o + 32 * k] = cf;
     }
   }
