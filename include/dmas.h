@@ -107,6 +107,10 @@ typedef struct {
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an
                                 envelope is requested without its raw image; 0 = 4 GiB         */
+  int32_t bf_engine;         /* beamform kernel: 0 = auto (the LDS.64 kernel -- paired root plane,
+                                one 8-byte shared load per 2 pixels -- when delays are integer and
+                                its windows fit two CTAs per SM, else the classic one); 1 = always
+                                the classic kernel.  Both give bit-identical images.           */
 } dmas_plan_desc;
 
 /* Fill `desc` with defaults (zero geometry; order 2; cf_eps 1e-30; lp 127 taps at 5 kHz;
@@ -156,6 +160,8 @@ typedef struct {
   int32_t psi_tile, t_tile;   /* beamform CTA tile: directions x samples                     */
   int32_t window;             /* staged samples per microphone per CTA (t_tile + tile spread) */
   int32_t chunk_frames;       /* frames per internal chunk                                   */
+  int32_t bf_kernel;          /* beamform kernel the plan launches: 0 classic (k_beamform), 1 LDS.64
+                                 (k_beamform_lds64), 2 microphone groups (k_beamform_mg)         */
 } dmas_plan_info;
 dmas_status dmas_get_plan_info(dmas_plan_t plan, dmas_plan_info* info);
 

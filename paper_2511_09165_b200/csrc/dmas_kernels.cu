@@ -71,30 +71,44 @@ __device__ __forceinline__ float signed_root(float v) {
   return copysignf(r, v);
 }
 
+// Paired plane (k_beamform_lds64, paired = 1): column j of a row holds the float2
+// (S[j], S[j + 32]), so the two samples a lane needs at pixels t and t + 32 are one 8-byte word
+// at column t + d for ANY delay d.  Sample t lands in component k of column t - 32k.
+__device__ __forceinline__ void store_root(float* S, int64_t row, int64_t Tp, int64_t G, int64_t t, float r,
+                                           int paired) {
+  if (!paired) {
+    S[row * Tp + G + t] = r;
+    return;
+  }
+  float* e = S + (row * Tp + G) * 2;
+  e[2 * t] = r;                                        // column t, component 0
+  e[2 * (t - BL_STRIDE) + 1] = r;                      // column t - 32, component 1
+}
+
 template <int P>
-__global__ void k_signed_roots(const float* __restrict__ m, float* __restrict__ S, int64_t T, int64_t Tp, int64_t G) {
+__global__ void k_signed_roots(const float* __restrict__ m, float* __restrict__ S, int64_t T, int64_t Tp, int64_t G,
+                               int paired) {
   const int64_t row = blockIdx.x;
   const float* mr = m + row * T;
-  float* sr = S + row * Tp + G;
   for (int64_t t = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.y * blockDim.x)
-    sr[t] = signed_root<P>(__ldg(mr + t));
+    store_root(S, row, Tp, G, t, signed_root<P>(__ldg(mr + t)), paired);
 }
 
 cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G,
-                                cudaStream_t st) {
+                                int paired, cudaStream_t st) {
   const int threads = 256;
   int64_t bx = (T + threads - 1) / threads;
   if (bx > 64) bx = 64;
   dim3 grid((unsigned)rows, (unsigned)bx);
   switch (order) {
-    case 1: k_signed_roots<1><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 2: k_signed_roots<2><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 3: k_signed_roots<3><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 4: k_signed_roots<4><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 5: k_signed_roots<5><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 6: k_signed_roots<6><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 7: k_signed_roots<7><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
-    case 8: k_signed_roots<8><<<grid, threads, 0, st>>>(m, S, T, Tp, G); break;
+    case 1: k_signed_roots<1><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 2: k_signed_roots<2><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 3: k_signed_roots<3><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 4: k_signed_roots<4><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 5: k_signed_roots<5><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 6: k_signed_roots<6><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 7: k_signed_roots<7><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
+    case 8: k_signed_roots<8><<<grid, threads, 0, st>>>(m, S, T, Tp, G, paired); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -110,7 +124,8 @@ cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t row
 template <int P>
 __global__ void __launch_bounds__(MF_THREADS) k_mf_roots(const float* __restrict__ raw, int64_t T_raw,
                                                          const float* __restrict__ w, int32_t Lp, float inv_energy,
-                                                         float* __restrict__ S, int64_t T, int64_t Tp, int64_t G) {
+                                                         float* __restrict__ S, int64_t T, int64_t Tp, int64_t G,
+                                                         int paired) {
   extern __shared__ __align__(16) float msm[];
   float* tw = msm;                                   // [Lp] taps
   float* win = msm + Lp;                             // [MF_T + Lp] raw window
@@ -138,27 +153,27 @@ __global__ void __launch_bounds__(MF_THREADS) k_mf_roots(const float* __restrict
       for (int j = 0; j < 4; ++j) acc[j] = fmaf(ww[r], v[j + r], acc[j]);
     cur = nxt;
   }
-  float* sr = S + row * Tp + G;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int64_t t = t0 + 4 * threadIdx.x + j;
-    if (t < T) sr[t] = signed_root<P>(acc[j] * inv_energy);
+    if (t < T) store_root(S, row, Tp, G, t, signed_root<P>(acc[j] * inv_energy), paired);
   }
 }
 
 cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const float* w, int32_t Lp, float inv_energy,
-                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, cudaStream_t st) {
+                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, int paired,
+                            cudaStream_t st) {
   dim3 grid((unsigned)rows, (unsigned)((T + MF_T - 1) / MF_T));
   const size_t smem = (size_t)(2 * Lp + MF_T) * sizeof(float);
   switch (order) {
-    case 1: k_mf_roots<1><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 2: k_mf_roots<2><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 3: k_mf_roots<3><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 4: k_mf_roots<4><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 5: k_mf_roots<5><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 6: k_mf_roots<6><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 7: k_mf_roots<7><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
-    case 8: k_mf_roots<8><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G); break;
+    case 1: k_mf_roots<1><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 2: k_mf_roots<2><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 3: k_mf_roots<3><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 4: k_mf_roots<4><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 5: k_mf_roots<5><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 6: k_mf_roots<6><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 7: k_mf_roots<7><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
+    case 8: k_mf_roots<8><<<grid, MF_THREADS, smem, st>>>(raw, T_raw, w, Lp, inv_energy, S, T, Tp, G, paired); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -671,10 +686,202 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform_mg(const BeamformArg
   if (q < npsi) bf_epilogue<P, KM>(a, acc, f, psi0 + q, t0, lane);
 }
 
+// ------------------------------------------------------------------------------------------
+// K3p — k_beamform_lds64 (integer delays, whole array staged): same tile (BF_PSI directions x
+// BF_T samples, one direction per warp at a time, lane pixels t0 + lane + 32k, k < 8), same
+// per-pixel arithmetic, microphone order and epilogue as k_beamform (bit-identical images), but
+// a lane fetches the samples of its pixels k and k + 1 with ONE LDS.64 from the paired plane
+// (column j = (S[j], S[j + 32])): the word for direction psi and mic i is column
+// t0 + lane + 64 m + d(psi, i), 8-byte aligned for any delay, lanes on consecutive columns
+// (conflict-free).  The accumulators are packed over those pixel pairs, so FADD2/FFMA2 take the
+// loaded pair as it lands: per (direction, mic) 4 LDS.64 + 1 IADD + 8 FMUL + 8 FADD2 + 8 FFMA2 =
+// 45 dispatch cycles for 8 pixels instead of k_beamform's ~50, at the same register count (so
+// the same 3 CTAs / 24 warps per SM).  Windows start at a per-(tile, mic) origin lo_i (even):
+// W = 224 + the largest per-mic spread columns of 8 B, one TMA bulk copy per microphone.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// Products of a pixel pair as two scalar IEEE multiplies: ptxas fuses a packed
+// mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2 despite the .rn modifiers (observed with
+// CUDA 12.9 for P3 += s^2 * s), which would round differently from acc_add<P>'s scalar
+// __fmul_rn; a scalar FMUL costs the same dispatch as half an FMUL2.
+__device__ __forceinline__ float2 mul2s(const float2& a, const float2& b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+
+// Accumulators of one pixel pair (.x = pixel k, .y = pixel k + 1).  Per lane and pixel the
+// operations are exactly acc_add<P>'s (same rounding), so get(h) reproduces the Acc<P> that
+// k_beamform holds for that pixel.
+template <int P> struct PAcc {                         // P >= 6: per-pixel scalar accumulators
+  Acc<P> px[2];
+  __device__ __forceinline__ void zero() { acc_zero<P>(px[0]); acc_zero<P>(px[1]); }
+  __device__ __forceinline__ void add2(const float2& v) { acc_add<P>(px[0], v.x); acc_add<P>(px[1], v.y); }
+  __device__ __forceinline__ Acc<P> get(int h) const { return px[h]; }
+};
+template <> struct PAcc<2> {
+  float2 p1, a, p2, b;
+  __device__ __forceinline__ void zero() { p1 = a = p2 = b = f2(0.f, 0.f); }
+  __device__ __forceinline__ void add2(const float2& s) {
+    const float2 x = f2(__fmul_rn(s.x, fabsf(s.x)), __fmul_rn(s.y, fabsf(s.y)));
+    p1 = __fadd2_rn(p1, s);                           // P1 += s
+    a = __fadd2_rn(a, x);                             // A  += x
+    p2 = __ffma2_rn(s, s, p2);                        // P2 += s^2 (= |x|)
+    b = __ffma2_rn(x, x, b);                          // B  += x^2
+  }
+  __device__ __forceinline__ Acc<2> get(int h) const {
+    Acc<2> c;
+    c.pa = h ? f2(p1.y, a.y) : f2(p1.x, a.x);
+    c.pb = h ? f2(p2.y, b.y) : f2(p2.x, b.x);
+    return c;
+  }
+};
+template <> struct PAcc<3> {
+  float2 p1, p2, a, b;
+  __device__ __forceinline__ void zero() { p1 = p2 = a = b = f2(0.f, 0.f); }
+  __device__ __forceinline__ void add2(const float2& s) {
+    const float2 s2 = mul2s(s, s);
+    const float2 x = mul2s(s2, s);
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, s2);
+    a = __fadd2_rn(a, x);                             // = P3
+    b = __ffma2_rn(x, x, b);
+  }
+  __device__ __forceinline__ Acc<3> get(int h) const {
+    Acc<3> c;
+    c.p12 = h ? f2(p1.y, p2.y) : f2(p1.x, p2.x);
+    c.a = h ? a.y : a.x;
+    c.b = h ? b.y : b.x;
+    return c;
+  }
+};
+template <> struct PAcc<4> {
+  float2 p1, p2, p3, p4, a, b;
+  __device__ __forceinline__ void zero() { p1 = p2 = p3 = p4 = a = b = f2(0.f, 0.f); }
+  __device__ __forceinline__ void add2(const float2& s) {
+    const float2 s2 = mul2s(s, s);
+    const float2 s3 = mul2s(s2, s);
+    const float2 s4 = mul2s(s2, s2);            // = |x|
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, s2);
+    p3 = __fadd2_rn(p3, s3);
+    p4 = __fadd2_rn(p4, s4);
+    a.x = fmaf(s3.x, fabsf(s.x), a.x);               // x = sgn(s) s^4
+    a.y = fmaf(s3.y, fabsf(s.y), a.y);
+    b = __ffma2_rn(s4, s4, b);
+  }
+  __device__ __forceinline__ Acc<4> get(int h) const {
+    Acc<4> c;
+    c.p12 = h ? f2(p1.y, p2.y) : f2(p1.x, p2.x);
+    c.p34 = h ? f2(p3.y, p4.y) : f2(p3.x, p4.x);
+    c.a = h ? a.y : a.x;
+    c.b = h ? b.y : b.x;
+    return c;
+  }
+};
+template <> struct PAcc<5> {
+  float2 p1, p2, p3, p4, a, b;
+  __device__ __forceinline__ void zero() { p1 = p2 = p3 = p4 = a = b = f2(0.f, 0.f); }
+  __device__ __forceinline__ void add2(const float2& s) {
+    const float2 s2 = mul2s(s, s);
+    const float2 s3 = mul2s(s2, s);
+    const float2 s4 = mul2s(s2, s2);
+    const float2 x = mul2s(s4, s);
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, s2);
+    p3 = __fadd2_rn(p3, s3);
+    p4 = __fadd2_rn(p4, s4);
+    a = __fadd2_rn(a, x);                             // = P5
+    b = __ffma2_rn(x, x, b);
+  }
+  __device__ __forceinline__ Acc<5> get(int h) const {
+    Acc<5> c;
+    c.p12 = h ? f2(p1.y, p2.y) : f2(p1.x, p2.x);
+    c.p34 = h ? f2(p3.y, p4.y) : f2(p3.x, p4.x);
+    c.a = h ? a.y : a.x;
+    c.b = h ? b.y : b.x;
+    return c;
+  }
+};
+
+template <int P, int KM>
+__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform_lds64(const BeamformArgs a) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const int32_t n_mics = a.n_mics, W = a.W;            // W = window columns (8 B) per mic
+  const int32_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
+  float* win = smem;                                   // [n_mics][W] float2 columns
+  float* zero = smem + (size_t)2 * n_mics * W;         // [BL_ZERO] float2 columns (padding mics)
+  int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * BL_ZERO);   // [BF_PSI][n_pad] byte offsets
+
+  const int64_t t0 = (int64_t)blockIdx.x * BF_T;
+  const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
+  const int64_t f = blockIdx.z;
+  const int npsi = (int)min((int64_t)BF_PSI, a.n_dirs - psi0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < 2 * BL_ZERO; j += BF_THREADS) zero[j] = 0.f;
+  __syncthreads();
+  if (warp == 0) {                                     // warp 0: one bulk copy per microphone
+    const uint32_t row_bytes = (uint32_t)W * 8u;
+    const uint32_t offs_bytes = (uint32_t)(BF_PSI * n_pad) * 4u;
+    if (lane == 0) {
+      mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes);
+      bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);
+    }
+    __syncwarp();
+    const int32_t* lo = a.q_lo + (size_t)blockIdx.y * n_mics;
+    const float* src0 = a.splane + ((f * n_mics) * a.Tp + a.G + t0) * 2;
+    for (int i = lane; i < n_mics; i += 32)
+      bulk_g2s(win + (size_t)i * W * 2, src0 + ((int64_t)i * a.Tp + __ldg(lo + i)) * 2, row_bytes, &bar);
+  }
+  mbar_wait(&bar, 0);
+
+  const uint32_t la = smem_u32(win) + 8u * (uint32_t)lane;
+  constexpr int U = bf_unroll<P>();
+  for (int q = warp; q < npsi; q += BF_WARPS) {
+    PAcc<P> acc[BF_KT / 2];
+#pragma unroll
+    for (int m = 0; m < BF_KT / 2; ++m) acc[m].zero();
+    const int4* o4 = reinterpret_cast<const int4*>(offs + q * n_pad);
+#pragma unroll 1
+    for (int j = 0; j < n_pad / 4; j += U / 4) {
+#pragma unroll
+      for (int u = 0; u < U / 4; ++u) {
+        const int4 o = o4[j + u];
+        const int oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t addr = la + (uint32_t)oo[h];      // byte offsets
+#pragma unroll
+          for (int m = 0; m < BF_KT / 2; ++m) acc[m].add2(lds_f32x2(addr + 512u * m));
+        }
+      }
+    }
+    Acc<P> px[BF_KT];                                  // pixel t0 + lane + 32 k
+#pragma unroll
+    for (int k = 0; k < BF_KT; ++k) px[k] = acc[k >> 1].get(k & 1);   // LDS m holds pixels 2m, 2m + 1
+    bf_epilogue<P, KM>(a, px, f, psi0 + q, t0, lane);
+  }
+}
+
 size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
   if (mg > 0) return (size_t)2 * mg * W * sizeof(float) + (size_t)BF_PSI_MG * n_mics * (interp ? 8 : 4);
   const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
   return ((size_t)n_mics * W + BF_ZERO) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
+}
+
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W) {
+  const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
+  return ((size_t)n_mics * W + BL_ZERO) * 8 + (size_t)BF_PSI * n_pad * 4;
 }
 
 template <int P>
@@ -689,6 +896,26 @@ static cudaError_t configure_order(int bytes) {
   if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 31, false>, attr, bytes))) return e;
   if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 4, true>, attr, bytes))) return e;
   return cudaFuncSetAttribute(k_beamform_mg<P, 31, true>, attr, bytes);
+}
+
+template <int P>
+static cudaError_t configure_order_lds64(int bytes) {
+  cudaError_t e;
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4>, attr, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform_lds64<P, 31>, attr, bytes);
+}
+
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W) {
+  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W);
+  cudaError_t e;
+  if ((e = configure_order_lds64<2>(bytes))) return e;
+  if ((e = configure_order_lds64<3>(bytes))) return e;
+  if ((e = configure_order_lds64<4>(bytes))) return e;
+  if ((e = configure_order_lds64<5>(bytes))) return e;
+  if ((e = configure_order_lds64<6>(bytes))) return e;
+  if ((e = configure_order_lds64<7>(bytes))) return e;
+  return configure_order_lds64<8>(bytes);
 }
 
 cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
@@ -706,6 +933,11 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t m
 template <int P>
 static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
+  if (a.q_lo) {                                        // paired plane, LDS.64 gathers
+    if (only_cfdmas) k_beamform_lds64<P, 4><<<grid, BF_THREADS, smem, st>>>(a);
+    else k_beamform_lds64<P, 31><<<grid, BF_THREADS, smem, st>>>(a);
+    return;
+  }
   if (a.mg > 0) {
     if (a.alpha) {
       if (only_cfdmas) k_beamform_mg<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
@@ -730,7 +962,8 @@ cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, 
   const int psi_tile = a.mg > 0 ? BF_PSI_MG : BF_PSI;
   const int64_t npt = (a.n_dirs + psi_tile - 1) / psi_tile;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
+  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W)
+                            : beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;
     case 3: launch_order<3>(a, grid, smem, st); break;

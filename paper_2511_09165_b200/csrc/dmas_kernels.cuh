@@ -29,6 +29,11 @@ constexpr int BF_UNROLL = DMAS_BF_UNROLL;   // interpolating / large-array paths
 constexpr int BF_MIC_PAD = 8;              // classic path: offset rows padded to 8 microphones
 constexpr int BF_ZERO = 32 * 8 + 4;        // zero block for padding microphones (+1 sample read when interpolating)
 constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per warp
+// LDS.64 path (k_beamform_lds64): paired plane column j = (S[j], S[j + BL_STRIDE]); a lane's
+// pixels k, k + 1 (t0 + lane + 32k) come from one column; the zero block covers the columns a
+// padding microphone's reads span (lanes 0..31 + 64 m, m < BF_KT / 2).
+constexpr int BL_STRIDE = 32;
+constexpr int BL_ZERO = 32 + 64 * (BF_KT / 2 - 1);
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
 constexpr int ENV_THREADS = 256;
@@ -55,8 +60,12 @@ struct BeamformArgs {
   const float* alpha;       // [n_dirs][n_mics] fractional delays in [0, 1) (linear pre-steering), or null
   int32_t mg;               // > 0: large-array path, microphones staged in groups of mg (tiles of BF_PSI_MG)
   int64_t Tp, G, T, n_dirs;
-  int32_t n_mics, W;        // W = staged samples per mic row (multiple of 4)
+  int32_t n_mics, W;        // W = staged samples per mic row (multiple of 4); LDS.64 path: columns
   float n_mics_f, cf_eps;
+  // LDS.64 path (q_lo != nullptr): splane is the paired plane [frames][n_mics][Tp][2] (column
+  // G + j holds (S[j], S[j + 32])); q_lo = per-(psi tile, mic) window origins in columns relative
+  // to t0 (even); offs = byte offsets 8 (i W + d - lo)
+  const int32_t* q_lo;      // [n_psi_tiles][n_mics]
 };
 
 struct LpTaps127 { float h[128]; };
@@ -69,18 +78,23 @@ cudaError_t launch_delay_table(const double* u /*[n_dirs][3]*/, const double* po
 
 // K2: S[f][i][G + t] = sgn(m) |m|^(1/p) for t in [0, T) (hoisted signed roots, A3); order 1 =
 // identity (the plane of m itself, used by the interpolating beamformer).
+// paired = 1 (LDS.64 beamform path): S is the paired plane [rows][Tp][2], sample t stored at
+// column G + t (component 0) and column G + t - 32 (component 1); G >= 32.
 cudaError_t launch_signed_roots(int order, const float* m, float* S, int64_t rows, int64_t T, int64_t Tp,
-                                int64_t G, cudaStream_t st);
+                                int64_t G, int paired, cudaStream_t st);
 
 // K0+K2: matched filter (correlation with the zero-padded chirp w[Lp], / energy) fused with the
 // signed roots; raw rows [rows][T_raw], T_raw >= T + L - 1 (NEXT-1).
 cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const float* w, int32_t Lp, float inv_energy,
-                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, cudaStream_t st);
+                            float* S, int64_t rows, int64_t T, int64_t Tp, int64_t G, int paired,
+                            cudaStream_t st);
 cudaError_t mf_configure(int32_t Lp);
 
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
 size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg);
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W);
 cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg);   // > 48 KB dynamic smem
 
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).

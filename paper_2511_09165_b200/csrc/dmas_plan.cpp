@@ -97,6 +97,8 @@ struct dmas_plan_s {
   float* d_alpha_tab = nullptr;       // classic interpolating path: per-tile padded fractions
   int32_t W = 0;                      // staged window per mic (beamform)
   int32_t mg = 0;                     // > 0: large-array path, microphones per staged group
+  int32_t paired = 0;                 // LDS.64 path: paired root plane, per-(tile, mic) windows
+  int32_t* d_qlo = nullptr;           // LDS.64 path: [n_psi_tiles][n_mics] window origins (columns)
   int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
   int32_t chunk_cap = 1;              // frames the signed-root plane holds
   float* d_splane = nullptr;
@@ -152,6 +154,7 @@ cudaError_t timed(dmas_plan_s* p, int kernel, cudaStream_t st, F&& fn) {
 void free_plan_memory(dmas_plan_s* p) {
   cudaFree(p->d_delays);
   cudaFree(p->d_tile_lo);
+  cudaFree(p->d_qlo);
   cudaFree(p->d_offs);
   cudaFree(p->d_alpha_tab);
   cudaFree(p->d_splane);
@@ -222,6 +225,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
   if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
+  if (d->bf_engine < 0 || d->bf_engine > 1) return fail(DMAS_ERR_INVALID, "bf_engine not in {0, 1}");
   if (d->delay_interp < 0 || d->delay_interp > 1) return fail(DMAS_ERR_INVALID, "delay_interp not in {0, 1}");
   if (d->mf_taps < 0 || d->mf_taps > dmas::MF_MAX_TAPS) return fail(DMAS_ERR_INVALID, "mf_taps not in [0, 16384]");
   if (d->mf_taps > 0 && !d->mf_coeffs) return fail(DMAS_ERR_NULL, "mf_coeffs is NULL");
@@ -259,12 +263,12 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   if (p->mf_taps > 0) {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
       return dmas::launch_mf_roots(p->interp ? 1 : p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
-                                   (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, st);
+                                   (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, p->paired, st);
     }));
   } else {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
       return dmas::launch_signed_roots(p->interp ? 1 : p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T,
-                                       p->Tp, p->G, st);
+                                       p->Tp, p->G, p->paired, st);
     }));
   }
   dmas::BeamformArgs a{};
@@ -284,6 +288,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.W = p->W;
   a.n_mics_f = (float)p->n_mics;
   a.cf_eps = p->cf_eps;
+  a.q_lo = p->d_qlo;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
   cudaStream_t es = st;
@@ -513,22 +518,77 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     mg = std::max<int64_t>(4, std::min<int64_t>(mg / 4 * 4, nm));
     p->mg = (int32_t)mg;
   }
-  const size_t smem = dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
+  // LDS.64 path (k_beamform_lds64): integer delays, whole array staged, and its windows (per
+  // (tile, mic) origin lo = min over the tile's directions of d, aligned down to even; W = 224 +
+  // the largest per-mic spread columns of 8 B) fit 3 CTAs per SM.
+  const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
+  std::vector<int32_t> qlo;
+  if (!p->interp && p->mg == 0 && desc->bf_engine == 0) {
+    const int64_t n_pt = (int64_t)tile_lo.size();
+    std::vector<int32_t> lo_t((size_t)n_pt * nm);
+    int32_t wmax = 0, lmin = INT32_MAX, lmax = INT32_MIN;
+    for (int64_t t = 0; t < n_pt; ++t) {
+      const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BF_PSI);
+      for (int i = 0; i < nm; ++i) {
+        int32_t lo = INT32_MAX, hi = INT32_MIN;
+        for (int64_t a = t * dmas::BF_PSI; a < a1; ++a) {
+          const int32_t v = p->h_delays[(size_t)a * nm + i];
+          lo = std::min(lo, v);
+          hi = std::max(hi, v);
+        }
+        const int32_t lo_al = (int32_t)(std::floor(lo / 2.0) * 2);
+        lo_t[(size_t)t * nm + i] = lo_al;
+        lmin = std::min(lmin, lo_al);
+        lmax = std::max(lmax, lo_al);
+        wmax = std::max(wmax, dmas::BL_ZERO + (hi - lo_al));
+      }
+    }
+    const int32_t Wp = (wmax + 1) / 2 * 2;
+    if (dmas::beamform_lds64_smem_bytes(nm, Wp) <= (size_t)74 * 1024) {   // 3 CTAs/SM, like k_beamform
+      p->paired = 1;
+      p->W = Wp;
+      qlo.swap(lo_t);
+      lo_min = lmin;
+      lo_max = lmax;
+    }
+  }
+  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W)
+                                : dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (smem + 64 > (size_t)smem_optin)
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
-  PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp, p->mg));
-  PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
-  PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  if (p->mg == 0) {
+  if (p->paired) {
+    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W));
+    // byte offsets into the CTA's [n_mics][W] window of 8-byte columns: 8 (i W + d - lo);
+    // padding microphones and directions past the grid end -> the zero block (column n_mics W)
+    const size_t n_pt = qlo.size() / nm;
+    const size_t n_tab = n_pt * dmas::BF_PSI * n_pad;
+    std::vector<int32_t> offs(n_tab, 8 * nm * p->W);
+    for (size_t t = 0; t < n_pt; ++t)
+      for (int q = 0; q < dmas::BF_PSI; ++q) {
+        const int64_t a = (int64_t)t * dmas::BF_PSI + q;
+        if (a >= nd) break;
+        const size_t row = ((size_t)t * dmas::BF_PSI + q) * n_pad;
+        for (int i = 0; i < nm; ++i)
+          offs[row + i] = 8 * (i * p->W + (p->h_delays[(size_t)a * nm + i] - qlo[t * nm + i]));
+      }
+    PLAN_TRY(cudaMalloc(&p->d_offs, n_tab * sizeof(int32_t)));
+    PLAN_TRY(cudaMemcpy(p->d_offs, offs.data(), n_tab * sizeof(int32_t), cudaMemcpyHostToDevice));
+    PLAN_TRY(cudaMalloc(&p->d_qlo, qlo.size() * sizeof(int32_t)));
+    PLAN_TRY(cudaMemcpy(p->d_qlo, qlo.data(), qlo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  } else {
+    PLAN_TRY(dmas::beamform_configure(nm, p->W, p->interp, p->mg));
+    PLAN_TRY(cudaMalloc(&p->d_tile_lo, tile_lo.size() * sizeof(int32_t)));
+    PLAN_TRY(cudaMemcpy(p->d_tile_lo, tile_lo.data(), tile_lo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  if (p->mg == 0 && !p->paired) {
     // classic path: every CTA of a psi tile (all t tiles, all frames) uses the same word offsets
     // i W + d - lo into its staged window (and, interpolating, the same fractions); build them once
     // here, the kernel TMA-copies its tile's [BF_PSI][n_pad] block(s) alongside the window.  Padding
     // microphones (and directions past the grid end) point at the kernel's zero block at word
     // n_mics W with fraction 0.
-    const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
     const size_t n_tab = tile_lo.size() * dmas::BF_PSI * n_pad;
     std::vector<int32_t> offs(n_tab, nm * p->W);
     std::vector<float> alph(p->interp ? n_tab : 0, 0.f);
@@ -551,13 +611,14 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   }
 
   // ---- signed-root plane with zero guards: reads at t + d outside [0, T) return 0 (reading Q5)
-  p->G = std::max<int64_t>(0, -(int64_t)lo_min);
+  // (LDS.64 path: columns of the paired plane; sample t is also stored at column G + t - 32)
+  p->G = std::max<int64_t>(p->paired ? dmas::BL_STRIDE : 0, -(int64_t)lo_min);
   p->G = (p->G + 3) / 4 * 4;
   const int64_t ntt = (p->T + dmas::BF_T - 1) / dmas::BF_T;
   p->Tp = p->G + (ntt - 1) * dmas::BF_T + std::max<int64_t>(0, lo_max) + p->W;
   p->Tp = std::max<int64_t>(p->Tp, p->G + p->T);
   p->Tp = (p->Tp + 3) / 4 * 4;
-  const size_t plane_frame = (size_t)nm * p->Tp * sizeof(float);
+  const size_t plane_frame = (size_t)nm * p->Tp * sizeof(float) * (p->paired ? 2 : 1);
   const size_t plane_budget = (size_t)256 << 20;
   p->chunk_cap = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)p->max_frames, plane_budget / plane_frame));
   PLAN_TRY(cudaMalloc(&p->d_splane, plane_frame * p->chunk_cap));
@@ -737,6 +798,7 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->t_tile = dmas::BF_T;
   info->window = p->W;
   info->chunk_frames = p->chunk_cap;
+  info->bf_kernel = p->paired ? 1 : p->mg > 0 ? 2 : 0;
   return DMAS_OK;
 }
 

@@ -64,6 +64,7 @@ class dmas_plan_desc(ctypes.Structure):
         ("delay_interp", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
+        ("bf_engine", ctypes.c_int32),
     ]
 
 
@@ -73,7 +74,7 @@ class dmas_plan_info(ctypes.Structure):
         ("n_mics", ctypes.c_int32), ("order", ctypes.c_int32), ("lp_taps", ctypes.c_int32),
         ("env_decim", ctypes.c_int32), ("device", ctypes.c_int32), ("d_min", ctypes.c_int32),
         ("d_max", ctypes.c_int32), ("psi_tile", ctypes.c_int32), ("t_tile", ctypes.c_int32),
-        ("window", ctypes.c_int32), ("chunk_frames", ctypes.c_int32),
+        ("window", ctypes.c_int32), ("chunk_frames", ctypes.c_int32), ("bf_kernel", ctypes.c_int32),
     ]
 
 
@@ -150,7 +151,7 @@ class Plan:
                  max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
                  device: int = -1, scratch_bytes: int = 0, env_engine: int = 0,
-                 mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0):
+                 mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0, bf_engine: int = 0):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -175,6 +176,7 @@ class Plan:
         d.env_decim, d.device, d.scratch_bytes = int(env_decim), int(device), int(scratch_bytes)
         d.env_engine = int(env_engine)
         d.delay_interp = int(delay_interp)
+        d.bf_engine = int(bf_engine)
         self.mf_taps = 0
         if mf_coeffs is not None and len(mf_coeffs) > 0:
             mf = np.ascontiguousarray(np.asarray(mf_coeffs, dtype=np.float32))

@@ -514,8 +514,54 @@ def test_large_array_parity(dm, kind):
     assert_parity(g[("raw", "cfdmas")], O.beamform_frame(sig[0], d0, p, alpha=al)["cfdmas"][None], f"{kind} linear")
 
 
-def test_classic_path_for_benchmark_configs(dm):
-    for name in ("C4", "C5"):
+def test_beamform_kernel_for_benchmark_configs(dm):
+    """C5 (32 mics, 32-direction tiles inside one elevation column) takes the LDS.64 kernel; C4
+    (64 mics) and C2 (tiles straddle elevation columns: wide per-mic spread) would fit fewer than
+    3 CTAs per SM and keep the classic kernel; bf_engine = 1 forces it."""
+    for name, k in (("C2", 0), ("C4", 0), ("C5", 1)):
         cfg = gen.config(name, frames=1)
         plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"])
-        assert plan.info["psi_tile"] == 32, (name, plan.info)
+        assert plan.info["psi_tile"] == 32 and plan.info["bf_kernel"] == k, (name, plan.info)
+        classic = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"], bf_engine=1)
+        assert classic.info["bf_kernel"] == 0
+
+
+# ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
+@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "ragged", "ragged_p6", "tiny", "short_T"])
+def test_lds64_kernel_bitwise_and_parity(dm, case):
+    """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
+    performs the same per-pixel operations in the same microphone order as the classic kernel:
+    images are bit-identical across ragged direction tiles (n_dirs % 32 != 0), ragged sample tiles
+    (T % 256 != 0), T shorter than the delay spread, every kind, orders 2..6; and within the
+    north_star bar of the oracle."""
+    import torch
+    what = what_all(dm)
+    if case.startswith("C5"):                               # C5's array, scene and grid: 300 directions
+        cfg = gen.config("C5", frames=2)                      # (9 full 32-direction tiles + 12), T = 4096
+        p = int(case[-1])
+        mic, dirs, sig = cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
+    elif case.startswith("ragged"):
+        p = 6 if case.endswith("p6") else 2
+        mic = gen.disk_array(24 if p == 6 else 13, 0.09, 5e-3, seed=61)
+        dirs = gen.az_el_grid(23, 85.0, 7, 55.0)            # 161 directions: 5 full tiles + 1
+        sig = gen.random_signals(2, len(mic), 601, seed=62, sparsity=0.2)   # 2 full 256-tiles + 89
+    elif case == "tiny":
+        p, mic, dirs = 3, gen.disk_array(5, 0.05, 5e-3, seed=63), gen.az_el_grid(3, 40.0, 1, 0.0)
+        sig = gen.random_signals(1, 5, 3, seed=64)
+    else:                                                    # T = 40 < delay spread (+-65)
+        p, mic, dirs = 2, gen.disk_array(32, seed=7), gen.az_el_grid(3, 30.0, 32, 50.0)
+        sig = gen.random_signals(2, 32, 40, seed=65, sparsity=0.1)
+    x = torch.from_numpy(np.ascontiguousarray(sig)).cuda()
+    res = []
+    for eng in (0, 1):
+        plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, sig.shape[2], max_frames=sig.shape[0], bf_engine=eng)
+        assert plan.info["bf_kernel"] == (1 if eng == 0 else 0), plan.info
+        r = plan.beamform(x, what)
+        torch.cuda.synchronize()
+        res.append({k: v.cpu().numpy() for k, v in r.items()})
+    for k in res[1]:
+        assert np.array_equal(res[0][k], res[1][k]), (case, k)
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
+    scale = math.comb(len(mic), p) * float(np.max(np.abs(sig))) + len(mic) * float(np.max(np.abs(sig)))
+    for key in ref:
+        assert_parity(res[0][key], ref[key], f"lds64 {case} {key}", zero_scale=scale)

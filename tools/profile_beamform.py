@@ -20,6 +20,7 @@ from workloads import gen  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--engine", type=int, default=0, help="bf_engine: 0 auto, 1 classic")
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--calls", type=int, default=3)
     ap.add_argument("--workload", default="C5")
@@ -29,7 +30,7 @@ def main():
     sig = torch.from_numpy(cfg["signals"]).cuda()
     sig = sig.repeat((args.frames + sig.shape[0] - 1) // sig.shape[0], 1, 1)[:args.frames].contiguous()
     plan = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"],
-                     max_frames=args.frames)
+                     max_frames=args.frames, bf_engine=args.engine)
     what = dmas.RAW(dmas.KIND_CFDMAS) if args.raw else dmas.ENV(dmas.KIND_CFDMAS)
     outs = None
     for c in range(args.calls):
