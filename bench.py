@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--workload", choices=["C5", "C4"], default="C5",
                     help="C5 = the metric's config (default); C4 = 64-mic p = 3 secondary line")
     ap.add_argument("--mode", choices=["weak", "dirshard"], default="weak")
+    ap.add_argument("--bf-engine", type=int, choices=[0, 1], default=0,
+                    help="beamform kernel: 0 auto (LDS.64 kernel where it fits), 1 classic k_beamform (comparison)")
     ap.add_argument("--interp", action="store_true",
                     help="linear-interpolation pre-steering (fractional delays, roots on the fly; NEXT-2)")
     ap.add_argument("--raw", action="store_true",
@@ -165,6 +167,7 @@ WORKLOADS = {
 # FP32-pipe lane-ops per microphone sample of k_beamform (acc_add<P>) and per pixel
 # epilogue (Newton-Girard + CF + CF product)
 OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
+BF_KERNELS = {0: "k_beamform", 1: "k_beamform_lds64", 2: "k_beamform_mg"}   # dmas_plan_info.bf_kernel
 OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
 
 
@@ -177,7 +180,8 @@ def config_dict(args, world):
             "mode": args.mode, "world": world, "l2": w["l2"],
             "input": "raw recordings, matched filter on the GPU (1125-tap chirp)" if args.raw
                      else "matched-filtered signals (north_star input)",
-            "presteer": "linear interpolation (fractional delays)" if args.interp else "nearest sample (integer LUT)"}
+            "presteer": "linear interpolation (fractional delays)" if args.interp else "nearest sample (integer LUT)",
+            "beamform_kernel": "classic k_beamform (forced)" if args.bf_engine == 1 else "auto"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -263,7 +267,8 @@ def run_ours(args, rank, world, local):
             x.copy_(torch.from_numpy(cfg["signals"]))
     F, T, p = args.frames, cfg["T"], cfg["order"]
     plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, max_frames=F, lp_taps=LP_TAPS, device=local,
-                     mf_coeffs=cfg.get("chirp") if args.raw else None, delay_interp=1 if args.interp else 0)
+                     mf_coeffs=cfg.get("chirp") if args.raw else None, delay_interp=1 if args.interp else 0, bf_engine=args.bf_engine)
+    bf_name = BF_KERNELS[plan.info["bf_kernel"]]
     what = dmas.ENV(dmas.KIND_CFDMAS)
     out = torch.empty((F, len(dirs), T), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -335,7 +340,7 @@ def run_ours(args, rank, world, local):
     traffic_launch = (tr["dram_bytes_per_launch"] * frames_launch / tr["frames_per_launch"]
                       if tr.get("dram_bytes_per_launch") and tr.get("frames_per_launch") else None)
     if dom == "beamform":
-        roofline = {"bound": "alu", "kernel": "k_beamform", "achieved": ach_bf, "peak": peak_top,
+        roofline = {"bound": "alu", "kernel": bf_name, "achieved": ach_bf, "peak": peak_top,
                     "unit": "Top/s (FP32 lane-ops)", "frac": ach_bf / peak_top}
     else:
         roofline = {"bound": "hbm", "kernel": "k_envelope_tc", "achieved": env_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -387,7 +392,7 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak" if args.mode == "weak" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded eRTIS-like point-reflector echoes, matched-filtered; workloads/gen.py)",
-            "config": config_dict(args, world), "frames_per_s": F * (world if args.mode == "weak" else 1) / (ms * 1e-3),
+            "config": dict(config_dict(args, world), beamform_kernel=bf_name), "frames_per_s": F * (world if args.mode == "weak" else 1) / (ms * 1e-3),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -549,7 +549,7 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         p, mic, dirs = 3, gen.disk_array(5, 0.05, 5e-3, seed=63), gen.az_el_grid(3, 40.0, 1, 0.0)
         sig = gen.random_signals(1, 5, 3, seed=64)
     else:                                                    # T = 40 < delay spread (+-65)
-        p, mic, dirs = 2, gen.disk_array(32, seed=7), gen.az_el_grid(3, 30.0, 32, 50.0)
+        p, mic, dirs = 2, gen.disk_array(32, seed=7), gen.az_el_grid(3, 30.0, 32, 10.0)
         sig = gen.random_signals(2, 32, 40, seed=65, sparsity=0.1)
     x = torch.from_numpy(np.ascontiguousarray(sig)).cuda()
     res = []
