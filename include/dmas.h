@@ -162,6 +162,9 @@ typedef struct {
   int32_t chunk_frames;       /* frames per internal chunk                                   */
   int32_t bf_kernel;          /* beamform kernel the plan launches: 0 classic (k_beamform), 1 LDS.64
                                  (k_beamform_lds64), 2 microphone groups (k_beamform_mg)         */
+  int32_t tile_order;         /* 0: CTA tiles are runs of consecutive directions; 1: compact
+                                 patches from recursive bisection of the unit vectors (LDS.64
+                                 path; images unaffected)                                        */
 } dmas_plan_info;
 dmas_status dmas_get_plan_info(dmas_plan_t plan, dmas_plan_info* info);
 

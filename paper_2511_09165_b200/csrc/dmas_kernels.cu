@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     Acc<P> px[BF_KT];                                  // pixel t0 + lane + 32 k
 #pragma unroll
     for (int k = 0; k < BF_KT; ++k) px[k] = acc[k >> 1].get(k & 1);   // LDS m holds pixels 2m, 2m + 1
-    bf_epilogue<P, KM>(a, px, f, psi0 + q, t0, lane);
+    bf_epilogue<P, KM>(a, px, f, a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q, t0, lane);
   }
 }
 

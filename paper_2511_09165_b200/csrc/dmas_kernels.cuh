@@ -66,6 +66,7 @@ struct BeamformArgs {
   // G + j holds (S[j], S[j + 32])); q_lo = per-(psi tile, mic) window origins in columns relative
   // to t0 (even); offs = byte offsets 8 (i W + d - lo)
   const int32_t* q_lo;      // [n_psi_tiles][n_mics]
+  const int32_t* psi_map;   // LDS.64 path: tile slot psi0 + q -> image row (k-d tiles), or null (identity)
 };
 
 struct LpTaps127 { float h[128]; };

@@ -75,6 +75,7 @@ class dmas_plan_info(ctypes.Structure):
         ("env_decim", ctypes.c_int32), ("device", ctypes.c_int32), ("d_min", ctypes.c_int32),
         ("d_max", ctypes.c_int32), ("psi_tile", ctypes.c_int32), ("t_tile", ctypes.c_int32),
         ("window", ctypes.c_int32), ("chunk_frames", ctypes.c_int32), ("bf_kernel", ctypes.c_int32),
+        ("tile_order", ctypes.c_int32),
     ]
 
 

@@ -515,19 +515,20 @@ def test_large_array_parity(dm, kind):
 
 
 def test_beamform_kernel_for_benchmark_configs(dm):
-    """C5 (32 mics, 32-direction tiles inside one elevation column) takes the LDS.64 kernel; C4
-    (64 mics) and C2 (tiles straddle elevation columns: wide per-mic spread) would fit fewer than
-    3 CTAs per SM and keep the classic kernel; bf_engine = 1 forces it."""
-    for name, k in (("C2", 0), ("C4", 0), ("C5", 1)):
+    """C5 and C2 (32 mics) take the LDS.64 kernel, C2 with k-d direction tiles (its consecutive rows
+    straddle its 30-direction elevation columns; the k-d patches fit 3 CTAs per SM); C4 (64 mics)
+    would fit fewer CTAs per SM than the classic kernel and keeps it; bf_engine = 1 forces it."""
+    for name, k, order in (("C2", 1, 1), ("C4", 0, 0), ("C5", 1, 0)):
         cfg = gen.config(name, frames=1)
         plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"])
         assert plan.info["psi_tile"] == 32 and plan.info["bf_kernel"] == k, (name, plan.info)
+        assert plan.info["tile_order"] == order, (name, plan.info)
         classic = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"], bf_engine=1)
         assert classic.info["bf_kernel"] == 0
 
 
 # ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
-@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "ragged", "ragged_p6", "tiny", "short_T"])
+@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "ragged", "ragged_p6", "tiny", "short_T"])
 def test_lds64_kernel_bitwise_and_parity(dm, case):
     """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
     performs the same per-pixel operations in the same microphone order as the classic kernel:
@@ -540,6 +541,9 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         cfg = gen.config("C5", frames=2)                      # (9 full 32-direction tiles + 12), T = 4096
         p = int(case[-1])
         mic, dirs, sig = cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
+    elif case == "C2p2":                                     # k-d tiles (rows scattered by psi_map)
+        cfg = gen.config("C2")
+        p, mic, dirs, sig = 2, cfg["mic_xyz"], cfg["dirs"], cfg["signals"]
     elif case.startswith("ragged"):
         p = 6 if case.endswith("p6") else 2
         mic = gen.disk_array(24 if p == 6 else 13, 0.09, 5e-3, seed=61)
