@@ -54,7 +54,10 @@ constexpr int OUT_BYTES = TILE_BLOCKS * ROW_BYTES;  // 16384
 #define DMAS_TC_NSTAGE 6
 #endif
 constexpr int NSTAGE = DMAS_TC_NSTAGE;
-constexpr int NOUT = 2;
+#ifndef DMAS_TC_NOUT
+#define DMAS_TC_NOUT 2
+#endif
+constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (TMA stores in flight)
 // warp roles
 constexpr int COPY_WARP0 = 0;                       // warps 0..3: shifted A copies -> TMEM (lane quarter = warp)
 constexpr int EPI_WARP0 = 4;                        // warps 4..7: TMEM accumulator -> clamp -> TMA store
