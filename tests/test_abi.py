@@ -95,6 +95,30 @@ def test_validation_errors(dm):
     assert _plan_err(dm, mf_coeffs=np.zeros(8)) == 2                                        # zero-energy chirp
     assert _plan_err(dm, mf_coeffs=np.ones(20000)) == 2                                     # too many taps
     assert _plan_err(dm, mf_coeffs=np.array([1.0, np.inf])) == 2
+    assert _plan_err(dm, bf_engine=2) == 2
+    assert _plan_err(dm, env_engine=2) == 2
+    assert _plan_err(dm, delay_interp=2) == 2
+
+
+def test_struct_layouts_match_header(dm):
+    """The ctypes mirrors of dmas_plan_desc / dmas_plan_info have the C compiler's layout: field
+    offsets and sizes from a tiny C program built against include/dmas.h."""
+    fields = {"dmas_plan_desc": dm.dmas_plan_desc, "dmas_plan_info": dm.dmas_plan_info}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "dmas.h"', 'int main(void){']
+    for sname, cls in fields.items():
+        src.append(f'printf("{sname} sizeof %zu\\n", sizeof({sname}));')
+        for fname, _ in cls._fields_:
+            src.append(f'printf("{sname} {fname} %zu\\n", offsetof({sname}, {fname}));')
+    src.append("return 0;}")
+    c, exe = "/tmp/_dmas_layout.c", "/tmp/_dmas_layout"
+    open(c, "w").write("\n".join(src) + "\n")
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l}
+    for sname, cls in fields.items():
+        assert got[(sname, "sizeof")] == ctypes.sizeof(cls), sname
+        for fname, _ in cls._fields_:
+            assert got[(sname, fname)] == getattr(cls, fname).offset, (sname, fname)
 
 
 def test_null_handling(dm):
