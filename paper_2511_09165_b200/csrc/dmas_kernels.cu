@@ -721,13 +721,19 @@ template <int P> struct PAcc {                         // P >= 6: per-pixel scal
   Acc<P> px[2];
   __device__ __forceinline__ void zero() { acc_zero<P>(px[0]); acc_zero<P>(px[1]); }
   __device__ __forceinline__ void add2(const float2& v) { acc_add<P>(px[0], v.x); acc_add<P>(px[1], v.y); }
+  __device__ __forceinline__ void add2x(const float2& s, const float2& x) {
+    acc_add_x<P>(px[0], s.x, x.x);
+    acc_add_x<P>(px[1], s.y, x.y);
+  }
   __device__ __forceinline__ Acc<P> get(int h) const { return px[h]; }
 };
 template <> struct PAcc<2> {
   float2 p1, a, p2, b;
   __device__ __forceinline__ void zero() { p1 = a = p2 = b = f2(0.f, 0.f); }
   __device__ __forceinline__ void add2(const float2& s) {
-    const float2 x = f2(__fmul_rn(s.x, fabsf(s.x)), __fmul_rn(s.y, fabsf(s.y)));
+    add2x(s, f2(__fmul_rn(s.x, fabsf(s.x)), __fmul_rn(s.y, fabsf(s.y))));
+  }
+  __device__ __forceinline__ void add2x(const float2& s, const float2& x) {   // = acc_add_x<2>
     p1 = __fadd2_rn(p1, s);                           // P1 += s
     a = __fadd2_rn(a, x);                             // A  += x
     p2 = __ffma2_rn(s, s, p2);                        // P2 += s^2 (= |x|)
@@ -749,6 +755,12 @@ template <> struct PAcc<3> {
     p1 = __fadd2_rn(p1, s);
     p2 = __fadd2_rn(p2, s2);
     a = __fadd2_rn(a, x);                             // = P3
+    b = __ffma2_rn(x, x, b);
+  }
+  __device__ __forceinline__ void add2x(const float2& s, const float2& x) {   // = acc_add_x<3>
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, mul2s(s, s));
+    a = __fadd2_rn(a, x);
     b = __ffma2_rn(x, x, b);
   }
   __device__ __forceinline__ Acc<3> get(int h) const {
@@ -774,6 +786,15 @@ template <> struct PAcc<4> {
     a.y = fmaf(s3.y, fabsf(s.y), a.y);
     b = __ffma2_rn(s4, s4, b);
   }
+  __device__ __forceinline__ void add2x(const float2& s, const float2& x) {   // = acc_add_x<4>
+    const float2 s2 = mul2s(s, s);
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, s2);
+    p3 = __fadd2_rn(p3, mul2s(s2, s));
+    p4 = __fadd2_rn(p4, f2(fabsf(x.x), fabsf(x.y)));   // P4 = sum |x|
+    a = __fadd2_rn(a, x);
+    b = __ffma2_rn(x, x, b);
+  }
   __device__ __forceinline__ Acc<4> get(int h) const {
     Acc<4> c;
     c.p12 = h ? f2(p1.y, p2.y) : f2(p1.x, p2.x);
@@ -798,6 +819,15 @@ template <> struct PAcc<5> {
     a = __fadd2_rn(a, x);                             // = P5
     b = __ffma2_rn(x, x, b);
   }
+  __device__ __forceinline__ void add2x(const float2& s, const float2& x) {   // = acc_add_x<5>
+    const float2 s2 = mul2s(s, s);
+    p1 = __fadd2_rn(p1, s);
+    p2 = __fadd2_rn(p2, s2);
+    p3 = __fadd2_rn(p3, mul2s(s2, s));
+    p4 = __fadd2_rn(p4, mul2s(s2, s2));
+    a = __fadd2_rn(a, x);
+    b = __ffma2_rn(x, x, b);
+  }
   __device__ __forceinline__ Acc<5> get(int h) const {
     Acc<5> c;
     c.p12 = h ? f2(p1.y, p2.y) : f2(p1.x, p2.x);
@@ -808,7 +838,12 @@ template <> struct PAcc<5> {
   }
 };
 
-template <int P, int KM>
+// INTERP (linear pre-steering, NEXT-2): the paired plane holds m itself, each (direction, mic)
+// carries a fraction alpha (plan-built table beside the offsets) and a lane reads columns c and
+// c + 1 — (m[t + d], m[t + d + 32]) and (m[t + d + 1], m[t + d + 33]) — i.e. both interpolation
+// neighbours of both pixels in two LDS.64 (k_beamform: two LDS per pixel); then exactly
+// k_beamform's x = fma(alpha, m1 - m0, m0), SFU root and acc_add_x per pixel.
+template <int P, int KM, bool INTERP>
 __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform_lds64(const BeamformArgs a) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
@@ -817,6 +852,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   float* win = smem;                                   // [n_mics][W] float2 columns
   float* zero = smem + (size_t)2 * n_mics * W;         // [BL_ZERO] float2 columns (padding mics)
   int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * BL_ZERO);   // [BF_PSI][n_pad] byte offsets
+  float* alph = reinterpret_cast<float*>(offs + BF_PSI * n_pad);     // [BF_PSI][n_pad] (INTERP)
 
   const int64_t t0 = (int64_t)blockIdx.x * BF_T;
   const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
@@ -834,8 +870,9 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     const uint32_t row_bytes = (uint32_t)W * 8u;
     const uint32_t offs_bytes = (uint32_t)(BF_PSI * n_pad) * 4u;
     if (lane == 0) {
-      mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes);
+      mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes * (INTERP ? 2u : 1u));
       bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);
+      if (INTERP) bulk_g2s(alph, a.alpha_tab + (size_t)blockIdx.y * BF_PSI * n_pad, offs_bytes, &bar);
     }
     __syncwarp();
     const int32_t* lo = a.q_lo + (size_t)blockIdx.y * n_mics;
@@ -852,17 +889,32 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
 #pragma unroll
     for (int m = 0; m < BF_KT / 2; ++m) acc[m].zero();
     const int4* o4 = reinterpret_cast<const int4*>(offs + q * n_pad);
+    const float4* a4 = reinterpret_cast<const float4*>(alph + q * n_pad);
+    constexpr int UU = INTERP ? 4 : U;
 #pragma unroll 1
-    for (int j = 0; j < n_pad / 4; j += U / 4) {
+    for (int j = 0; j < n_pad / 4; j += UU / 4) {
 #pragma unroll
-      for (int u = 0; u < U / 4; ++u) {
+      for (int u = 0; u < UU / 4; ++u) {
         const int4 o = o4[j + u];
         const int oo[4] = {o.x, o.y, o.z, o.w};
+        float al[4] = {0.f, 0.f, 0.f, 0.f};
+        if (INTERP) {
+          const float4 av = a4[j + u];
+          al[0] = av.x; al[1] = av.y; al[2] = av.z; al[3] = av.w;
+        }
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const uint32_t addr = la + (uint32_t)oo[h];      // byte offsets
 #pragma unroll
-          for (int m = 0; m < BF_KT / 2; ++m) acc[m].add2(lds_f32x2(addr + 512u * m));
+          for (int m = 0; m < BF_KT / 2; ++m) {
+            if (INTERP) {
+              const float2 m0 = lds_f32x2(addr + 512u * m), m1 = lds_f32x2(addr + 512u * m + 8u);
+              const float2 x = f2(fmaf(al[h], m1.x - m0.x, m0.x), fmaf(al[h], m1.y - m0.y, m0.y));   // reading Q4b
+              acc[m].add2x(f2(root_fast<P>(x.x), root_fast<P>(x.y)), x);
+            } else {
+              acc[m].add2(lds_f32x2(addr + 512u * m));
+            }
+          }
         }
       }
     }
@@ -879,9 +931,9 @@ size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
   return ((size_t)n_mics * W + BF_ZERO) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
-size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W) {
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp) {
   const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
-  return ((size_t)n_mics * W + BL_ZERO) * 8 + (size_t)BF_PSI * n_pad * 4;
+  return ((size_t)n_mics * W + BL_ZERO) * 8 + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
 template <int P>
@@ -902,12 +954,14 @@ template <int P>
 static cudaError_t configure_order_lds64(int bytes) {
   cudaError_t e;
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4>, attr, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform_lds64<P, 31>, attr, bytes);
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, false>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, true>, attr, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform_lds64<P, 31, true>, attr, bytes);
 }
 
-cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W) {
-  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp) {
+  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp);
   cudaError_t e;
   if ((e = configure_order_lds64<2>(bytes))) return e;
   if ((e = configure_order_lds64<3>(bytes))) return e;
@@ -934,8 +988,13 @@ template <int P>
 static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
   if (a.q_lo) {                                        // paired plane, LDS.64 gathers
-    if (only_cfdmas) k_beamform_lds64<P, 4><<<grid, BF_THREADS, smem, st>>>(a);
-    else k_beamform_lds64<P, 31><<<grid, BF_THREADS, smem, st>>>(a);
+    if (a.alpha) {
+      if (only_cfdmas) k_beamform_lds64<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<P, 31, true><<<grid, BF_THREADS, smem, st>>>(a);
+    } else {
+      if (only_cfdmas) k_beamform_lds64<P, 4, false><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<P, 31, false><<<grid, BF_THREADS, smem, st>>>(a);
+    }
     return;
   }
   if (a.mg > 0) {
@@ -962,7 +1021,7 @@ cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, 
   const int psi_tile = a.mg > 0 ? BF_PSI_MG : BF_PSI;
   const int64_t npt = (a.n_dirs + psi_tile - 1) / psi_tile;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W)
+  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W, a.alpha != nullptr)
                             : beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;

@@ -33,7 +33,8 @@ constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per w
 // pixels k, k + 1 (t0 + lane + 32k) come from one column; the zero block covers the columns a
 // padding microphone's reads span (lanes 0..31 + 64 m, m < BF_KT / 2).
 constexpr int BL_STRIDE = 32;
-constexpr int BL_ZERO = 32 + 64 * (BF_KT / 2 - 1);
+constexpr int BL_SPAN = 32 + 64 * (BF_KT / 2 - 1);      // columns a zero-delay-spread window spans
+constexpr int BL_ZERO = BL_SPAN + 2;                      // (+1 column read when interpolating, +1 for 16 B)
 
 // Envelope CTA tile (K4 fast path): 1024 outputs of one row, 4 consecutive outputs / thread.
 constexpr int ENV_THREADS = 256;
@@ -94,8 +95,8 @@ cudaError_t mf_configure(int32_t Lp);
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
 size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg);
-size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W);
-cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W);
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp);
 cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg);   // > 48 KB dynamic smem
 
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).

@@ -532,7 +532,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   // through psi_map (the image layout is unchanged).
   const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
   std::vector<int32_t> qlo, order;
-  if (!p->interp && p->mg == 0 && desc->bf_engine == 0) {
+  if (p->mg == 0 && desc->bf_engine == 0) {
     const int64_t n_pt = (int64_t)tile_lo.size();
     auto eval = [&](const std::vector<int32_t>* ord, std::vector<int32_t>& lo_t, int32_t& wmax, int32_t& lmin,
                     int32_t& lmax) {
@@ -554,7 +554,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
           lo_t[(size_t)t * nm + i] = lo_al;
           lmin = std::min(lmin, lo_al);
           lmax = std::max(lmax, lo_al);
-          wmax = std::max(wmax, dmas::BL_ZERO + (hi - lo_al));
+          wmax = std::max(wmax, dmas::BL_SPAN + (hi - lo_al) + (p->interp ? 1 : 0));   // + m[j + 1]
         }
       }
     };
@@ -596,10 +596,10 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     const size_t budget = p->order == 2 ? (size_t)74 * 1024 : p->order <= 5 ? (size_t)110 * 1024 : (size_t)220 * 1024;
     // consecutive rows when they fit (measured 1-3% faster than k-d tiles of a narrower window on
     // C5), k-d tiles only when they are what makes the window fit
-    const bool use_kd = dmas::beamform_lds64_smem_bytes(nm, (w_n + 1) / 2 * 2) > budget && w_k < w_n;
+    const bool use_kd = dmas::beamform_lds64_smem_bytes(nm, (w_n + 1) / 2 * 2, p->interp) > budget && w_k < w_n;
     const int32_t wmax = use_kd ? w_k : w_n;
     const int32_t Wp = (wmax + 1) / 2 * 2;
-    if (dmas::beamform_lds64_smem_bytes(nm, Wp) <= budget) {
+    if (dmas::beamform_lds64_smem_bytes(nm, Wp, p->interp) <= budget) {
       p->paired = 1;
       p->W = Wp;
       if (use_kd) {
@@ -614,7 +614,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       }
     }
   }
-  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W)
+  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W, p->interp)
                                 : dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -622,23 +622,31 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
   if (p->paired) {
-    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W));
+    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W, p->interp));
     // byte offsets into the CTA's [n_mics][W] window of 8-byte columns: 8 (i W + d - lo);
     // padding microphones and directions past the grid end -> the zero block (column n_mics W)
     const size_t n_pt = qlo.size() / nm;
     const size_t n_tab = n_pt * dmas::BF_PSI * n_pad;
+    // (interpolating: the fractions alongside, padding 0)
     std::vector<int32_t> offs(n_tab, 8 * nm * p->W);
+    std::vector<float> alph(p->interp ? n_tab : 0, 0.f);
     for (size_t t = 0; t < n_pt; ++t)
       for (int q = 0; q < dmas::BF_PSI; ++q) {
         const int64_t k = (int64_t)t * dmas::BF_PSI + q;
         if (k >= nd) break;
         const int64_t a = order.empty() ? k : order[(size_t)k];
         const size_t row = ((size_t)t * dmas::BF_PSI + q) * n_pad;
-        for (int i = 0; i < nm; ++i)
+        for (int i = 0; i < nm; ++i) {
           offs[row + i] = 8 * (i * p->W + (p->h_delays[(size_t)a * nm + i] - qlo[t * nm + i]));
+          if (p->interp) alph[row + i] = p->h_alpha[(size_t)a * nm + i];
+        }
       }
     PLAN_TRY(cudaMalloc(&p->d_offs, n_tab * sizeof(int32_t)));
     PLAN_TRY(cudaMemcpy(p->d_offs, offs.data(), n_tab * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (p->interp) {
+      PLAN_TRY(cudaMalloc(&p->d_alpha_tab, n_tab * sizeof(float)));
+      PLAN_TRY(cudaMemcpy(p->d_alpha_tab, alph.data(), n_tab * sizeof(float), cudaMemcpyHostToDevice));
+    }
     PLAN_TRY(cudaMalloc(&p->d_qlo, qlo.size() * sizeof(int32_t)));
     PLAN_TRY(cudaMemcpy(p->d_qlo, qlo.data(), qlo.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     if (!order.empty()) {

@@ -528,7 +528,8 @@ def test_beamform_kernel_for_benchmark_configs(dm):
 
 
 # ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
-@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "ragged", "ragged_p6", "tiny", "short_T"])
+@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "ragged", "ragged_p6", "tiny", "short_T",
+                                  "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
 def test_lds64_kernel_bitwise_and_parity(dm, case):
     """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
     performs the same per-pixel operations in the same microphone order as the classic kernel:
@@ -537,6 +538,8 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
     north_star bar of the oracle."""
     import torch
     what = what_all(dm)
+    interp = case.endswith("i")                               # linear pre-steering (NEXT-2)
+    case = case[:-1] if interp else case
     if case.startswith("C5"):                               # C5's array, scene and grid: 300 directions
         cfg = gen.config("C5", frames=2)                      # (9 full 32-direction tiles + 12), T = 4096
         p = int(case[-1])
@@ -545,7 +548,7 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         cfg = gen.config("C2")
         p, mic, dirs, sig = 2, cfg["mic_xyz"], cfg["dirs"], cfg["signals"]
     elif case.startswith("ragged"):
-        p = 6 if case.endswith("p6") else 2
+        p = 6 if case.endswith("p6") else 2 if not interp else 3
         mic = gen.disk_array(24 if p == 6 else 13, 0.09, 5e-3, seed=61)
         dirs = gen.az_el_grid(23, 85.0, 7, 55.0)            # 161 directions: 5 full tiles + 1
         sig = gen.random_signals(2, len(mic), 601, seed=62, sparsity=0.2)   # 2 full 256-tiles + 89
@@ -558,14 +561,26 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
     x = torch.from_numpy(np.ascontiguousarray(sig)).cuda()
     res = []
     for eng in (0, 1):
-        plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, sig.shape[2], max_frames=sig.shape[0], bf_engine=eng)
+        plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, sig.shape[2], max_frames=sig.shape[0], bf_engine=eng,
+                       delay_interp=1 if interp else 0)
         assert plan.info["bf_kernel"] == (1 if eng == 0 else 0), plan.info
         r = plan.beamform(x, what)
         torch.cuda.synchronize()
         res.append({k: v.cpu().numpy() for k, v in r.items()})
     for k in res[1]:
-        assert np.array_equal(res[0][k], res[1][k]), (case, k)
-    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
+        assert np.array_equal(res[0][k], res[1][k]), (case, interp, k)
+    if interp:
+        d0, al = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND, mode="linear")
+        ref = {}
+        h = O.lpf_taps()
+        for f in range(sig.shape[0]):
+            img = O.beamform_frame(sig[f], d0, p, alpha=al)
+            for k in KINDS:
+                ref.setdefault(("raw", k), []).append(img[k])
+                ref.setdefault(("env", k), []).append(O.envelope(img[k], h))
+        ref = {k: np.stack(v) for k, v in ref.items()}
+    else:
+        ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, env_kinds=KINDS)
     scale = math.comb(len(mic), p) * float(np.max(np.abs(sig))) + len(mic) * float(np.max(np.abs(sig)))
     for key in ref:
         assert_parity(res[0][key], ref[key], f"lds64 {case} {key}", zero_scale=scale)
