@@ -542,10 +542,10 @@ __device__ __forceinline__ void bf_accumulate_padded(Acc<P> (&acc)[BF_KT], uint3
 // Newton-Girard + CF epilogue and coalesced stores of one direction's 8 pixels.
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
-template <int P, int KM>
-__device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> (&acc)[BF_KT], int64_t f, int64_t psi,
+template <int P, int KM, int KT = BF_KT>
+__device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> (&acc)[KT], int64_t f, int64_t psi,
                                             int64_t t0, int lane) {
-  const bool full_t = t0 + BF_T <= a.T;
+  const bool full_t = t0 + 32 * KT <= a.T;
   const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
   if (KM == 4 && full_t) {
     // streaming CF-DMAS request, whole tile in range: no per-pixel guards; for p = 2 the 1/2 of
@@ -554,7 +554,7 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     float* dst = a.out[2] + o;
     const float n2 = (P == 2 ? 2.f : 1.f) * a.n_mics_f, e2 = (P == 2 ? 2.f : 1.f) * a.cf_eps;
 #pragma unroll
-    for (int k = 0; k < BF_KT; ++k) {
+    for (int k = 0; k < KT; ++k) {
       float A, B, E;
       acc_final_cfdmas<P>(acc[k], A, B, E);
       dst[32 * k] = FM(E, FM(FM(A, A), rcp_approx(fmaf(n2, B, e2))));
@@ -562,7 +562,7 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     return;
   }
 #pragma unroll
-  for (int k = 0; k < BF_KT; ++k) {
+  for (int k = 0; k < KT; ++k) {
     if (!full_t && t0 + lane + 32 * k >= a.T) continue;
     float A, B, E;
     acc_final<P>(acc[k], A, B, E);
@@ -843,18 +843,19 @@ template <> struct PAcc<5> {
 // c + 1 — (m[t + d], m[t + d + 32]) and (m[t + d + 1], m[t + d + 33]) — i.e. both interpolation
 // neighbours of both pixels in two LDS.64 (k_beamform: two LDS per pixel); then exactly
 // k_beamform's x = fma(alpha, m1 - m0, m0), SFU root and acc_add_x per pixel.
-template <int P, int KM, bool INTERP>
-__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? 2 : 1)) k_beamform_lds64(const BeamformArgs a) {
+template <int P, int KM, bool INTERP, int KT>
+__global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ? (KT == 4 ? 3 : 2) : 1)) k_beamform_lds64(const BeamformArgs a) {
+  constexpr int ZC = bl_zero(KT);                      // zero-block columns
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar;
   const int32_t n_mics = a.n_mics, W = a.W;            // W = window columns (8 B) per mic
   const int32_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
   float* win = smem;                                   // [n_mics][W] float2 columns
-  float* zero = smem + (size_t)2 * n_mics * W;         // [BL_ZERO] float2 columns (padding mics)
-  int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * BL_ZERO);   // [BF_PSI][n_pad] byte offsets
+  float* zero = smem + (size_t)2 * n_mics * W;         // [ZC] float2 columns (padding mics)
+  int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * ZC);   // [BF_PSI][n_pad] byte offsets
   float* alph = reinterpret_cast<float*>(offs + BF_PSI * n_pad);     // [BF_PSI][n_pad] (INTERP)
 
-  const int64_t t0 = (int64_t)blockIdx.x * BF_T;
+  const int64_t t0 = (int64_t)blockIdx.x * (32 * KT);
   const int64_t psi0 = (int64_t)blockIdx.y * BF_PSI;
   const int64_t f = blockIdx.z;
   const int npsi = (int)min((int64_t)BF_PSI, a.n_dirs - psi0);
@@ -864,7 +865,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = threadIdx.x; j < 2 * BL_ZERO; j += BF_THREADS) zero[j] = 0.f;
+  for (int j = threadIdx.x; j < 2 * ZC; j += BF_THREADS) zero[j] = 0.f;
   __syncthreads();
   if (warp == 0) {                                     // warp 0: one bulk copy per microphone
     const uint32_t row_bytes = (uint32_t)W * 8u;
@@ -885,9 +886,9 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   const uint32_t la = smem_u32(win) + 8u * (uint32_t)lane;
   constexpr int U = bf_unroll<P>();
   for (int q = warp; q < npsi; q += BF_WARPS) {
-    PAcc<P> acc[BF_KT / 2];
+    PAcc<P> acc[KT / 2];
 #pragma unroll
-    for (int m = 0; m < BF_KT / 2; ++m) acc[m].zero();
+    for (int m = 0; m < KT / 2; ++m) acc[m].zero();
     const int4* o4 = reinterpret_cast<const int4*>(offs + q * n_pad);
     const float4* a4 = reinterpret_cast<const float4*>(alph + q * n_pad);
     constexpr int UU = INTERP ? 4 : U;
@@ -906,7 +907,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
         for (int h = 0; h < 4; ++h) {
           const uint32_t addr = la + (uint32_t)oo[h];      // byte offsets
 #pragma unroll
-          for (int m = 0; m < BF_KT / 2; ++m) {
+          for (int m = 0; m < KT / 2; ++m) {
             if (INTERP) {
               const float2 m0 = lds_f32x2(addr + 512u * m), m1 = lds_f32x2(addr + 512u * m + 8u);
               const float2 x = f2(fmaf(al[h], m1.x - m0.x, m0.x), fmaf(al[h], m1.y - m0.y, m0.y));   // reading Q4b
@@ -918,10 +919,10 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
         }
       }
     }
-    Acc<P> px[BF_KT];                                  // pixel t0 + lane + 32 k
+    Acc<P> px[KT];                                  // pixel t0 + lane + 32 k
 #pragma unroll
-    for (int k = 0; k < BF_KT; ++k) px[k] = acc[k >> 1].get(k & 1);   // LDS m holds pixels 2m, 2m + 1
-    bf_epilogue<P, KM>(a, px, f, a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q, t0, lane);
+    for (int k = 0; k < KT; ++k) px[k] = acc[k >> 1].get(k & 1);   // LDS m holds pixels 2m, 2m + 1
+    bf_epilogue<P, KM, KT>(a, px, f, a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q, t0, lane);
   }
 }
 
@@ -931,9 +932,9 @@ size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
   return ((size_t)n_mics * W + BF_ZERO) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
-size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp) {
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t kt) {
   const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
-  return ((size_t)n_mics * W + BL_ZERO) * 8 + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
+  return ((size_t)n_mics * W + bl_zero(kt)) * 8 + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
 template <int P>
@@ -954,14 +955,16 @@ template <int P>
 static cudaError_t configure_order_lds64(int bytes) {
   cudaError_t e;
   const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, true>, attr, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform_lds64<P, 31, true>, attr, bytes);
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false, 8>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, false, 8>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, true, 8>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, true, 8>, attr, bytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false, 4>, attr, bytes))) return e;
+  return cudaFuncSetAttribute(k_beamform_lds64<P, 31, false, 4>, attr, bytes);
 }
 
-cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp) {
-  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt) {
+  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp, kt);
   cudaError_t e;
   if ((e = configure_order_lds64<2>(bytes))) return e;
   if ((e = configure_order_lds64<3>(bytes))) return e;
@@ -989,11 +992,14 @@ static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStre
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
   if (a.q_lo) {                                        // paired plane, LDS.64 gathers
     if (a.alpha) {
-      if (only_cfdmas) k_beamform_lds64<P, 4, true><<<grid, BF_THREADS, smem, st>>>(a);
-      else k_beamform_lds64<P, 31, true><<<grid, BF_THREADS, smem, st>>>(a);
+      if (only_cfdmas) k_beamform_lds64<P, 4, true, 8><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<P, 31, true, 8><<<grid, BF_THREADS, smem, st>>>(a);
+    } else if (a.kt == 4) {
+      if (only_cfdmas) k_beamform_lds64<P, 4, false, 4><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<P, 31, false, 4><<<grid, BF_THREADS, smem, st>>>(a);
     } else {
-      if (only_cfdmas) k_beamform_lds64<P, 4, false><<<grid, BF_THREADS, smem, st>>>(a);
-      else k_beamform_lds64<P, 31, false><<<grid, BF_THREADS, smem, st>>>(a);
+      if (only_cfdmas) k_beamform_lds64<P, 4, false, 8><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<P, 31, false, 8><<<grid, BF_THREADS, smem, st>>>(a);
     }
     return;
   }
@@ -1017,11 +1023,12 @@ static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStre
 }
 
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
-  const int64_t ntt = (a.T + BF_T - 1) / BF_T;
+  const int t_tile = a.q_lo ? 32 * a.kt : BF_T;
+  const int64_t ntt = (a.T + t_tile - 1) / t_tile;
   const int psi_tile = a.mg > 0 ? BF_PSI_MG : BF_PSI;
   const int64_t npt = (a.n_dirs + psi_tile - 1) / psi_tile;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W, a.alpha != nullptr)
+  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.kt)
                             : beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;

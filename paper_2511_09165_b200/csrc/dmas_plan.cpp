@@ -98,6 +98,7 @@ struct dmas_plan_s {
   int32_t W = 0;                      // staged window per mic (beamform)
   int32_t mg = 0;                     // > 0: large-array path, microphones per staged group
   int32_t paired = 0;                 // LDS.64 path: paired root plane, per-(tile, mic) windows
+  int32_t lds_kt = 8;                 // LDS.64 path: pixels per lane (8: 256-sample tiles, 4: 128)
   int32_t* d_qlo = nullptr;           // LDS.64 path: [n_psi_tiles][n_mics] window origins (columns)
   int32_t* d_psi_map = nullptr;       // LDS.64 path: tile slot -> image row (k-d tiles), or null
   int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
@@ -292,6 +293,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.cf_eps = p->cf_eps;
   a.q_lo = p->d_qlo;
   a.psi_map = p->d_psi_map;
+  a.kt = p->lds_kt;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
   cudaStream_t es = st;
@@ -554,7 +556,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
           lo_t[(size_t)t * nm + i] = lo_al;
           lmin = std::min(lmin, lo_al);
           lmax = std::max(lmax, lo_al);
-          wmax = std::max(wmax, dmas::BL_SPAN + (hi - lo_al) + (p->interp ? 1 : 0));   // + m[j + 1]
+          wmax = std::max(wmax, hi - lo_al);           // spread; window = bl_span(kt) + spread (+1)
         }
       }
     };
@@ -592,16 +594,32 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       }
     }
     eval(&kd_ord, lo_k, w_k, lmin_k, lmax_k);
-    // the CTAs per SM k_beamform gets (launch bounds: 3 at p = 2, 2 at p = 3..5, 1 above)
-    const size_t budget = p->order == 2 ? (size_t)74 * 1024 : p->order <= 5 ? (size_t)110 * 1024 : (size_t)220 * 1024;
-    // consecutive rows when they fit (measured 1-3% faster than k-d tiles of a narrower window on
-    // C5), k-d tiles only when they are what makes the window fit
-    const bool use_kd = dmas::beamform_lds64_smem_bytes(nm, (w_n + 1) / 2 * 2, p->interp) > budget && w_k < w_n;
-    const int32_t wmax = use_kd ? w_k : w_n;
-    const int32_t Wp = (wmax + 1) / 2 * 2;
-    if (dmas::beamform_lds64_smem_bytes(nm, Wp, p->interp) <= budget) {
-      p->paired = 1;
-      p->W = Wp;
+    // Pick the tile: 8 pixels per lane (256-sample tiles) when its windows fit as many CTAs per SM
+    // as k_beamform gets (launch bounds: 3 at p = 2, 2 at p = 3..5, 1 above), else 4 pixels per
+    // lane (128-sample tiles, 3 CTAs per SM; integer delays, p <= 5) — 64-microphone arrays (C4).
+    // Consecutive rows when they fit (measured 1-3% faster than k-d tiles of a narrower window on
+    // C5), k-d tiles only when they are what makes the window fit.
+    const int extra = p->interp ? 1 : 0;                 // + m[j + 1]
+    bool use_kd = false;
+    for (int kt : {8, 4}) {
+      if (kt == 4 && (p->interp || p->order > 5)) continue;
+      const size_t budget = (p->order == 2 || kt == 4) ? (size_t)74 * 1024
+                            : p->order <= 5 ? (size_t)110 * 1024 : (size_t)220 * 1024;
+      const int32_t wn = (dmas::bl_span(kt) + w_n + extra + 1) / 2 * 2;
+      const int32_t wk = (dmas::bl_span(kt) + w_k + extra + 1) / 2 * 2;
+      if (dmas::beamform_lds64_smem_bytes(nm, wn, p->interp, kt) <= budget) {
+        p->paired = 1;
+        p->lds_kt = kt;
+        p->W = wn;
+      } else if (w_k < w_n && dmas::beamform_lds64_smem_bytes(nm, wk, p->interp, kt) <= budget) {
+        p->paired = 1;
+        p->lds_kt = kt;
+        p->W = wk;
+        use_kd = true;
+      }
+      if (p->paired) break;
+    }
+    if (p->paired) {
       if (use_kd) {
         qlo.swap(lo_k);
         order.swap(kd_ord);
@@ -614,7 +632,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       }
     }
   }
-  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W, p->interp)
+  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W, p->interp, p->lds_kt)
                                 : dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -622,7 +640,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
   if (p->paired) {
-    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W, p->interp));
+    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W, p->interp, p->lds_kt));
     // byte offsets into the CTA's [n_mics][W] window of 8-byte columns: 8 (i W + d - lo);
     // padding microphones and directions past the grid end -> the zero block (column n_mics W)
     const size_t n_pt = qlo.size() / nm;
@@ -689,8 +707,9 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   // (LDS.64 path: columns of the paired plane; sample t is also stored at column G + t - 32)
   p->G = std::max<int64_t>(p->paired ? dmas::BL_STRIDE : 0, -(int64_t)lo_min);
   p->G = (p->G + 3) / 4 * 4;
-  const int64_t ntt = (p->T + dmas::BF_T - 1) / dmas::BF_T;
-  p->Tp = p->G + (ntt - 1) * dmas::BF_T + std::max<int64_t>(0, lo_max) + p->W;
+  const int t_tile = p->paired ? 32 * p->lds_kt : dmas::BF_T;
+  const int64_t ntt = (p->T + t_tile - 1) / t_tile;
+  p->Tp = p->G + (ntt - 1) * t_tile + std::max<int64_t>(0, lo_max) + p->W;
   p->Tp = std::max<int64_t>(p->Tp, p->G + p->T);
   p->Tp = (p->Tp + 3) / 4 * 4;
   const size_t plane_frame = (size_t)nm * p->Tp * sizeof(float) * (p->paired ? 2 : 1);
@@ -870,7 +889,7 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->d_min = p->dmin;
   info->d_max = p->dmax;
   info->psi_tile = p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
-  info->t_tile = dmas::BF_T;
+  info->t_tile = p->paired ? 32 * p->lds_kt : dmas::BF_T;
   info->window = p->W;
   info->chunk_frames = p->chunk_cap;
   info->bf_kernel = p->paired ? 1 : p->mg > 0 ? 2 : 0;

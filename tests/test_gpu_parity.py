@@ -515,21 +515,22 @@ def test_large_array_parity(dm, kind):
 
 
 def test_beamform_kernel_for_benchmark_configs(dm):
-    """C5 and C2 (32 mics) take the LDS.64 kernel, C2 with k-d direction tiles (its consecutive rows
-    straddle its 30-direction elevation columns; the k-d patches fit 3 CTAs per SM); C4 (64 mics)
-    would fit fewer CTAs per SM than the classic kernel and keeps it; bf_engine = 1 forces it."""
-    for name, k, order in (("C2", 1, 1), ("C4", 0, 0), ("C5", 1, 0)):
+    """All three take the LDS.64 kernel: C5 with 256-sample tiles of consecutive rows; C2 with k-d
+    direction tiles (its consecutive rows straddle its 30-direction elevation columns); C4 (64 mics)
+    with 128-sample k-d tiles (4 pixels per lane: the 256-sample windows of 64 microphones would
+    not fit 2 CTAs per SM).  bf_engine = 1 forces the classic kernel."""
+    for name, k, order, tt in (("C2", 1, 1, 256), ("C4", 1, 1, 128), ("C5", 1, 0, 256)):
         cfg = gen.config(name, frames=1)
         plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"])
         assert plan.info["psi_tile"] == 32 and plan.info["bf_kernel"] == k, (name, plan.info)
-        assert plan.info["tile_order"] == order, (name, plan.info)
+        assert plan.info["tile_order"] == order and plan.info["t_tile"] == tt, (name, plan.info)
         classic = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"], bf_engine=1)
         assert classic.info["bf_kernel"] == 0
 
 
 # ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
-@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "ragged", "ragged_p6", "tiny", "short_T",
-                                  "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
+@pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "C4p3", "C4p5", "ragged", "ragged_p6", "tiny",
+                                  "short_T", "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
 def test_lds64_kernel_bitwise_and_parity(dm, case):
     """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
     performs the same per-pixel operations in the same microphone order as the classic kernel:
@@ -544,6 +545,9 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         cfg = gen.config("C5", frames=2)                      # (9 full 32-direction tiles + 12), T = 4096
         p = int(case[-1])
         mic, dirs, sig = cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
+    elif case.startswith("C4"):                             # 64 mics: 4 pixels per lane, k-d tiles
+        cfg = gen.config("C4", frames=1)
+        p, mic, dirs, sig = int(case[-1]), cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
     elif case == "C2p2":                                     # k-d tiles (rows scattered by psi_map)
         cfg = gen.config("C2")
         p, mic, dirs, sig = 2, cfg["mic_xyz"], cfg["dirs"], cfg["signals"]
