@@ -659,6 +659,19 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
           if (p->interp) alph[row + i] = p->h_alpha[(size_t)a * nm + i];
         }
       }
+    // bounds audit (compute-sanitizer is unavailable on the GPU pool): a lane reads columns
+    // off / 8 + lane + 64 m (+ 1 interpolating), m < kt / 2, which must stay inside the microphone's
+    // own window row, or inside the zero block for padding slots
+    {
+      const int64_t reach = dmas::bl_span(p->lds_kt) - 1 + (p->interp ? 1 : 0);
+      for (size_t e = 0; e < n_tab; ++e) {
+        const int64_t col = offs[e] / 8, i = col / p->W;
+        const bool pad = col == (int64_t)nm * p->W;
+        if (col < 0 || (!pad && (i >= nm || col - i * p->W + reach >= p->W)) ||
+            (pad && reach >= dmas::bl_zero(p->lds_kt)))
+          return bail(fail(DMAS_ERR_INVALID, "internal: LDS.64 offset table leaves its window"));
+      }
+    }
     PLAN_TRY(cudaMalloc(&p->d_offs, n_tab * sizeof(int32_t)));
     PLAN_TRY(cudaMemcpy(p->d_offs, offs.data(), n_tab * sizeof(int32_t), cudaMemcpyHostToDevice));
     if (p->interp) {
@@ -712,6 +725,9 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   p->Tp = p->G + (ntt - 1) * t_tile + std::max<int64_t>(0, lo_max) + p->W;
   p->Tp = std::max<int64_t>(p->Tp, p->G + p->T);
   p->Tp = (p->Tp + 3) / 4 * 4;
+  // bounds audit: every staged window [G + t0 + lo, + W) lies inside a plane row
+  if (p->mg == 0 && (p->G + lo_min < 0 || p->G + (ntt - 1) * t_tile + lo_max + p->W > p->Tp))
+    return bail(fail(DMAS_ERR_INVALID, "internal: staged window leaves the root plane"));
   const size_t plane_frame = (size_t)nm * p->Tp * sizeof(float) * (p->paired ? 2 : 1);
   const size_t plane_budget = (size_t)256 << 20;
   p->chunk_cap = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)p->max_frames, plane_budget / plane_frame));

@@ -1,6 +1,7 @@
 """Run every kernel path once on small inputs (for compute-sanitizer / quick checks on a GPU box):
 nearest and linear pre-steering, orders 2..8, tensor-core / FP32 / generic envelopes, band-pass,
-decimation, matched filter, host pipeline, ragged shapes."""
+decimation, matched filter, host pipeline, ragged shapes, every beamform kernel (classic, LDS.64
+with consecutive / k-d tiles and 8 / 4 pixels per lane, microphone groups)."""
 import os
 import sys
 
@@ -27,6 +28,21 @@ def main():
                 plan = dmas.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, T, max_frames=2, **kw)
                 plan.beamform(sig, allk)
                 plan.beamform(sig, dmas.ENV(dmas.KIND_CFDMAS))
+                plan.close()
+    # classic kernel (forced), LDS.64 k-d tiles (an elevation-fastest grid whose columns straddle
+    # tiles) and LDS.64 with 4 pixels per lane (64 microphones), large-array microphone groups
+    for mic_n, grid, kw in ((16, gen.az_el_grid(9, 60.0, 5, 30.0), {"bf_engine": 1}),
+                            (32, gen.az_el_grid(12, 90.0, 30, 45.0), {}),
+                            (64, gen.az_el_grid(8, 90.0, 40, 60.0), {}),
+                            (160, gen.az_el_grid(5, 60.0, 3, 20.0), {})):
+        m = gen.disk_array(mic_n, 0.10, 4e-3 if mic_n <= 64 else 3.5e-3, seed=mic_n)
+        for T in (1024 + 96, 301):
+            sig = torch.from_numpy(gen.random_signals(1, mic_n, T, seed=T + mic_n)).cuda()
+            for p in (2, 3):
+                plan = dmas.Plan(m, grid, gen.FS, gen.C_SOUND, p, T, max_frames=1, **kw)
+                plan.beamform(sig, allk)
+                print(f"  mics {mic_n} T {T} p {p}: bf_kernel {plan.info['bf_kernel']} tile_order "
+                      f"{plan.info['tile_order']} t_tile {plan.info['t_tile']}")
                 plan.close()
     cfg = gen.raw_config("C1", frames=2)
     plan = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=1,
