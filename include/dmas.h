@@ -158,7 +158,9 @@ typedef struct {
   int32_t n_mics, order, lp_taps, env_decim, device;
   int32_t d_min, d_max;       /* range of the delay table (samples)                          */
   int32_t psi_tile, t_tile;   /* beamform CTA tile: directions x samples                     */
-  int32_t window;             /* staged samples per microphone per CTA (t_tile + tile spread) */
+  int32_t window;             /* staged columns per microphone per CTA: samples (classic kernel:
+                                 t_tile + tile spread) or 8-byte sample pairs (LDS.64 kernel:
+                                 t_tile - 32 + per-microphone spread)                           */
   int32_t chunk_frames;       /* frames per internal chunk                                   */
   int32_t bf_kernel;          /* beamform kernel the plan launches: 0 classic (k_beamform), 1 LDS.64
                                  (k_beamform_lds64), 2 microphone groups (k_beamform_mg)         */
