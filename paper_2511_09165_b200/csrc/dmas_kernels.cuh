@@ -35,6 +35,10 @@ constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per w
 constexpr int BL_STRIDE = 32;
 // kt = pixels per lane (8: 256-sample tiles; 4: 128-sample tiles for arrays whose 8-pixel windows
 // would not fit the CTAs per SM, e.g. 64 microphones)
+#ifndef DMAS_BL_PSI
+#define DMAS_BL_PSI 32
+#endif
+constexpr int BL_PSI = DMAS_BL_PSI;        // directions per LDS.64 tile (BF_WARPS x directions per warp)
 __host__ __device__ constexpr int bl_span(int kt) { return 32 + 64 * (kt / 2 - 1); }   // window columns at 0 spread
 __host__ __device__ constexpr int bl_zero(int kt) { return bl_span(kt) + 2; }   // (+1 read when interpolating, +1 for 16 B)
 

@@ -535,7 +535,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
   std::vector<int32_t> qlo, order;
   if (p->mg == 0 && desc->bf_engine == 0) {
-    const int64_t n_pt = (int64_t)tile_lo.size();
+    const int64_t n_pt = (nd + dmas::BL_PSI - 1) / dmas::BL_PSI;
     auto eval = [&](const std::vector<int32_t>* ord, std::vector<int32_t>& lo_t, int32_t& wmax, int32_t& lmin,
                     int32_t& lmax) {
       lo_t.assign((size_t)n_pt * nm, 0);
@@ -543,10 +543,10 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       lmin = INT32_MAX;
       lmax = INT32_MIN;
       for (int64_t t = 0; t < n_pt; ++t) {
-        const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BF_PSI);
+        const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BL_PSI);
         for (int i = 0; i < nm; ++i) {
           int32_t lo = INT32_MAX, hi = INT32_MIN;
-          for (int64_t k = t * dmas::BF_PSI; k < a1; ++k) {
+          for (int64_t k = t * dmas::BL_PSI; k < a1; ++k) {
             const int64_t a = ord ? (*ord)[(size_t)k] : k;
             const int32_t v = p->h_delays[(size_t)a * nm + i];
             lo = std::min(lo, v);
@@ -567,7 +567,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       // k-d grouping: split the set at a multiple of 32 along the unit-vector component with
       // the largest range, recursively, so every tile but the last holds exactly 32 directions
       for (int64_t a = 0; a < nd; ++a) kd_ord[(size_t)a] = (int32_t)a;
-      const int64_t G = dmas::BF_PSI;
+      const int64_t G = dmas::BL_PSI;
       std::vector<std::pair<int64_t, int64_t>> stack{{0, nd}};
       while (!stack.empty()) {
         const auto [b, e] = stack.back();
@@ -644,16 +644,16 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     // byte offsets into the CTA's [n_mics][W] window of 8-byte columns: 8 (i W + d - lo);
     // padding microphones and directions past the grid end -> the zero block (column n_mics W)
     const size_t n_pt = qlo.size() / nm;
-    const size_t n_tab = n_pt * dmas::BF_PSI * n_pad;
+    const size_t n_tab = n_pt * dmas::BL_PSI * n_pad;
     // (interpolating: the fractions alongside, padding 0)
     std::vector<int32_t> offs(n_tab, 8 * nm * p->W);
     std::vector<float> alph(p->interp ? n_tab : 0, 0.f);
     for (size_t t = 0; t < n_pt; ++t)
-      for (int q = 0; q < dmas::BF_PSI; ++q) {
-        const int64_t k = (int64_t)t * dmas::BF_PSI + q;
+      for (int q = 0; q < dmas::BL_PSI; ++q) {
+        const int64_t k = (int64_t)t * dmas::BL_PSI + q;
         if (k >= nd) break;
         const int64_t a = order.empty() ? k : order[(size_t)k];
-        const size_t row = ((size_t)t * dmas::BF_PSI + q) * n_pad;
+        const size_t row = ((size_t)t * dmas::BL_PSI + q) * n_pad;
         for (int i = 0; i < nm; ++i) {
           offs[row + i] = 8 * (i * p->W + (p->h_delays[(size_t)a * nm + i] - qlo[t * nm + i]));
           if (p->interp) alph[row + i] = p->h_alpha[(size_t)a * nm + i];
@@ -904,7 +904,7 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->device = p->device;
   info->d_min = p->dmin;
   info->d_max = p->dmax;
-  info->psi_tile = p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
+  info->psi_tile = p->paired ? dmas::BL_PSI : p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
   info->t_tile = p->paired ? 32 * p->lds_kt : dmas::BF_T;
   info->window = p->W;
   info->chunk_frames = p->chunk_cap;
