@@ -601,7 +601,10 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     // C5), k-d tiles only when they are what makes the window fit.
     const int extra = p->interp ? 1 : 0;                 // + m[j + 1]
     bool use_kd = false;
-    for (int kt : {8, 4}) {
+#ifndef DMAS_LDS_KT4_FIRST
+#define DMAS_LDS_KT4_FIRST 0
+#endif
+    for (int kt : {DMAS_LDS_KT4_FIRST ? 4 : 8, DMAS_LDS_KT4_FIRST ? 8 : 4}) {
       if (kt == 4 && (p->interp || p->order > 5)) continue;
       const size_t budget = (p->order == 2 || kt == 4) ? (size_t)74 * 1024
                             : p->order <= 5 ? (size_t)110 * 1024 : (size_t)220 * 1024;
