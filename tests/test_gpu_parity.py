@@ -530,7 +530,7 @@ def test_beamform_kernel_for_benchmark_configs(dm):
 
 # ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
 @pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "C4p3", "C4p5", "ragged", "ragged_p6", "tiny",
-                                  "short_T", "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
+                                  "short_T", "scattered", "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
 def test_lds64_kernel_bitwise_and_parity(dm, case):
     """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
     performs the same per-pixel operations in the same microphone order as the classic kernel:
@@ -548,6 +548,11 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
     elif case.startswith("C4"):                             # 64 mics: 4 pixels per lane, k-d tiles
         cfg = gen.config("C4", frames=1)
         p, mic, dirs, sig = int(case[-1]), cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
+    elif case == "scattered":                                # 500 random directions in random order:
+        cfg = gen.config("C5", frames=1)                      # only k-d tiles can fit the window
+        rng = np.random.default_rng(66)
+        dirs = np.stack([rng.uniform(-1.2, 1.2, 500), rng.uniform(-0.9, 0.9, 500)], axis=1)
+        p, mic, sig = 2, cfg["mic_xyz"], cfg["signals"][:, :, :1024].copy()
     elif case == "C2p2":                                     # k-d tiles (rows scattered by psi_map)
         cfg = gen.config("C2")
         p, mic, dirs, sig = 2, cfg["mic_xyz"], cfg["dirs"], cfg["signals"]
@@ -568,6 +573,8 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, sig.shape[2], max_frames=sig.shape[0], bf_engine=eng,
                        delay_interp=1 if interp else 0)
         assert plan.info["bf_kernel"] == (1 if eng == 0 else 0), plan.info
+        if case == "scattered" and eng == 0:
+            assert plan.info["tile_order"] == 1, plan.info
         r = plan.beamform(x, what)
         torch.cuda.synchronize()
         res.append({k: v.cpu().numpy() for k, v in r.items()})
