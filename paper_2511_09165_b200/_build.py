@@ -39,14 +39,31 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (the translation units are independent),
+    then link the shared library; same flags as command()."""
     if not force and up_to_date():
         return LIB
-    cmd = command()
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+    base = command()
+    flags = [a for a in base[1:base.index("-o")] if a != "-shared"]
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc_path(), *flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((obj, subprocess.Popen(cmd)))
+    objs = []
+    for obj, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, "nvcc " + obj)
+        objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd[cmd.index("-o") + 1] = tmp
-    subprocess.run(cmd, check=True)
+    link = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    if verbose:
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(tmp, LIB)
     return LIB
 
