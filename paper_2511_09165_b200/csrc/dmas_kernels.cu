@@ -561,21 +561,41 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     }
     return;
   }
+  if (KM == 4) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      if (!full_t && t0 + lane + 32 * k >= a.T) continue;
+      float A, B, E;
+      acc_final<P>(acc[k], A, B, E);
+      a.out[2][o + 32 * k] = FM(E, FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps))));
+    }
+    return;
+  }
+  // generic request: the CF (a reciprocal per pixel) only when a CF-weighted kind is asked for
+  // (warp-uniform branch); values identical either way
+  const bool want_cf = a.out[2] || a.out[3] || a.out[4];
+  if (!want_cf) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      if (!full_t && t0 + lane + 32 * k >= a.T) continue;
+      float A, B, E;
+      acc_final<P>(acc[k], A, B, E);
+      if (a.out[0]) a.out[0][o + 32 * k] = A;
+      if (a.out[1]) a.out[1][o + 32 * k] = E;
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < KT; ++k) {
     if (!full_t && t0 + lane + 32 * k >= a.T) continue;
     float A, B, E;
     acc_final<P>(acc[k], A, B, E);
     const float cf = FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps)));
-    if (KM == 4) {
-      a.out[2][o + 32 * k] = FM(E, cf);
-    } else {
-      if (a.out[0]) a.out[0][o + 32 * k] = A;
-      if (a.out[1]) a.out[1][o + 32 * k] = E;
-      if (a.out[2]) a.out[2][o + 32 * k] = FM(E, cf);
-      if (a.out[3]) a.out[3][o + 32 * k] = FM(A, cf);
-      if (a.out[4]) a.out[4][o + 32 * k] = cf;
-    }
+    if (a.out[0]) a.out[0][o + 32 * k] = A;
+    if (a.out[1]) a.out[1][o + 32 * k] = E;
+    if (a.out[2]) a.out[2][o + 32 * k] = FM(E, cf);
+    if (a.out[3]) a.out[3][o + 32 * k] = FM(A, cf);
+    if (a.out[4]) a.out[4][o + 32 * k] = cf;
   }
 }
 
