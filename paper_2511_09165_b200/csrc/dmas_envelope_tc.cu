@@ -51,11 +51,11 @@ constexpr int ROW_BYTES = BLK * 4;                  // 128 B per block row (fp32
 constexpr int STAGE_BYTES = 17408;                  // 132 * 128 rounded up to 1024 (swizzle atom)
 constexpr int OUT_BYTES = TILE_BLOCKS * ROW_BYTES;  // 16384
 #ifndef DMAS_TC_NSTAGE
-#define DMAS_TC_NSTAGE 6
+#define DMAS_TC_NSTAGE 4
 #endif
 constexpr int NSTAGE = DMAS_TC_NSTAGE;
 #ifndef DMAS_TC_NOUT
-#define DMAS_TC_NOUT 2
+#define DMAS_TC_NOUT 4
 #endif
 constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (TMA stores in flight)
 // warp roles

@@ -911,7 +911,10 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     for (int m = 0; m < KT / 2; ++m) acc[m].zero();
     const int4* o4 = reinterpret_cast<const int4*>(offs + q * n_pad);
     const float4* a4 = reinterpret_cast<const float4*>(alph + q * n_pad);
-    constexpr int UU = INTERP ? 4 : U;
+#ifndef DMAS_LDS_UNROLL
+#define DMAS_LDS_UNROLL 0
+#endif
+    constexpr int UU = INTERP ? 4 : DMAS_LDS_UNROLL > 0 ? DMAS_LDS_UNROLL : U;   // microphones per iteration
 #pragma unroll 1
     for (int j = 0; j < n_pad / 4; j += UU / 4) {
 #pragma unroll
