@@ -872,13 +872,14 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   const int32_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
   float* win = smem;                                   // [n_mics][W] float2 columns
   float* zero = smem + (size_t)2 * n_mics * W;         // [ZC] float2 columns (padding mics)
-  int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * ZC);   // [BL_PSI][n_pad] byte offsets
-  float* alph = reinterpret_cast<float*>(offs + BL_PSI * n_pad);     // [BL_PSI][n_pad] (INTERP)
+  const int32_t QP = a.l_psi;                          // directions per tile (64 or 32)
+  int32_t* offs = reinterpret_cast<int32_t*>(zero + 2 * ZC);   // [QP][n_pad] byte offsets
+  float* alph = reinterpret_cast<float*>(offs + QP * n_pad);     // [QP][n_pad] (INTERP)
 
   const int64_t t0 = (int64_t)blockIdx.x * (32 * KT);
-  const int64_t psi0 = (int64_t)blockIdx.y * BL_PSI;
+  const int64_t psi0 = (int64_t)blockIdx.y * QP;
   const int64_t f = blockIdx.z;
-  const int npsi = (int)min((int64_t)BL_PSI, a.n_dirs - psi0);
+  const int npsi = (int)min((int64_t)QP, a.n_dirs - psi0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -889,11 +890,11 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   __syncthreads();
   if (warp == 0) {                                     // warp 0: one bulk copy per microphone
     const uint32_t row_bytes = (uint32_t)W * 8u;
-    const uint32_t offs_bytes = (uint32_t)(BL_PSI * n_pad) * 4u;
+    const uint32_t offs_bytes = (uint32_t)(QP * n_pad) * 4u;
     if (lane == 0) {
       mbar_expect_tx(&bar, row_bytes * (uint32_t)n_mics + offs_bytes * (INTERP ? 2u : 1u));
-      bulk_g2s(offs, a.offs + (size_t)blockIdx.y * BL_PSI * n_pad, offs_bytes, &bar);
-      if (INTERP) bulk_g2s(alph, a.alpha_tab + (size_t)blockIdx.y * BL_PSI * n_pad, offs_bytes, &bar);
+      bulk_g2s(offs, a.offs + (size_t)blockIdx.y * QP * n_pad, offs_bytes, &bar);
+      if (INTERP) bulk_g2s(alph, a.alpha_tab + (size_t)blockIdx.y * QP * n_pad, offs_bytes, &bar);
     }
     __syncwarp();
     const int32_t* lo = a.q_lo + (size_t)blockIdx.y * n_mics;
@@ -957,9 +958,9 @@ size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
   return ((size_t)n_mics * W + BF_ZERO) * sizeof(float) + (size_t)BF_PSI * n_pad * 4 * (interp ? 2 : 1);
 }
 
-size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t kt) {
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi) {
   const size_t n_pad = (n_mics + BF_MIC_PAD - 1) / BF_MIC_PAD * BF_MIC_PAD;
-  return ((size_t)n_mics * W + bl_zero(kt)) * 8 + (size_t)BL_PSI * n_pad * 4 * (interp ? 2 : 1);
+  return ((size_t)n_mics * W + bl_zero(kt)) * 8 + (size_t)psi * n_pad * 4 * (interp ? 2 : 1);
 }
 
 template <int P>
@@ -988,8 +989,8 @@ static cudaError_t configure_order_lds64(int bytes) {
   return cudaFuncSetAttribute(k_beamform_lds64<P, 31, false, 4>, attr, bytes);
 }
 
-cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt) {
-  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp, kt);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi) {
+  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp, kt, psi);
   cudaError_t e;
   if ((e = configure_order_lds64<2>(bytes))) return e;
   if ((e = configure_order_lds64<3>(bytes))) return e;
@@ -1050,10 +1051,10 @@ static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStre
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st) {
   const int t_tile = a.q_lo ? 32 * a.kt : BF_T;
   const int64_t ntt = (a.T + t_tile - 1) / t_tile;
-  const int psi_tile = a.q_lo ? BL_PSI : a.mg > 0 ? BF_PSI_MG : BF_PSI;
+  const int psi_tile = a.q_lo ? a.l_psi : a.mg > 0 ? BF_PSI_MG : BF_PSI;
   const int64_t npt = (a.n_dirs + psi_tile - 1) / psi_tile;
   dim3 grid((unsigned)ntt, (unsigned)npt, (unsigned)n_frames);
-  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.kt)
+  const size_t smem = a.q_lo ? beamform_lds64_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.kt, a.l_psi)
                             : beamform_smem_bytes(a.n_mics, a.W, a.alpha != nullptr, a.mg);
   switch (order) {
     case 2: launch_order<2>(a, grid, smem, st); break;

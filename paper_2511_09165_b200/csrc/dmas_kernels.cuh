@@ -35,10 +35,6 @@ constexpr int BF_PSI_MG = BF_WARPS;     // large-array path: one direction per w
 constexpr int BL_STRIDE = 32;
 // kt = pixels per lane (8: 256-sample tiles; 4: 128-sample tiles for arrays whose 8-pixel windows
 // would not fit the CTAs per SM, e.g. 64 microphones)
-#ifndef DMAS_BL_PSI
-#define DMAS_BL_PSI 32
-#endif
-constexpr int BL_PSI = DMAS_BL_PSI;        // directions per LDS.64 tile (BF_WARPS x directions per warp)
 __host__ __device__ constexpr int bl_span(int kt) { return 32 + 64 * (kt / 2 - 1); }   // window columns at 0 spread
 __host__ __device__ constexpr int bl_zero(int kt) { return bl_span(kt) + 2; }   // (+1 read when interpolating, +1 for 16 B)
 
@@ -75,6 +71,7 @@ struct BeamformArgs {
   const int32_t* q_lo;      // [n_psi_tiles][n_mics]
   const int32_t* psi_map;   // LDS.64 path: tile slot psi0 + q -> image row (k-d tiles), or null (identity)
   int32_t kt;               // LDS.64 path: pixels per lane (8 or 4; 4 only without interpolation)
+  int32_t l_psi;            // LDS.64 path: directions per tile (64 or 32)
 };
 
 struct LpTaps127 { float h[128]; };
@@ -102,8 +99,8 @@ cudaError_t mf_configure(int32_t Lp);
 // K3: gather + power sums + Newton-Girard + CF (A2-A4).  grid = (t tiles, psi tiles, frames).
 cudaError_t launch_beamform(int order, const BeamformArgs& a, int32_t n_frames, cudaStream_t st);
 size_t beamform_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t mg);
-size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t kt);
-cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt);
+size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi);
+cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi);
 cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg);   // > 48 KB dynamic smem
 
 // K4: [band-pass] -> |.| -> low-pass -> clamp >= 0 -> decimate (A5), one row per (frame, psi).

@@ -99,6 +99,7 @@ struct dmas_plan_s {
   int32_t mg = 0;                     // > 0: large-array path, microphones per staged group
   int32_t paired = 0;                 // LDS.64 path: paired root plane, per-(tile, mic) windows
   int32_t lds_kt = 8;                 // LDS.64 path: pixels per lane (8: 256-sample tiles, 4: 128)
+  int32_t lds_psi = 32;               // LDS.64 path: directions per tile (64 or 32)
   int32_t* d_qlo = nullptr;           // LDS.64 path: [n_psi_tiles][n_mics] window origins (columns)
   int32_t* d_psi_map = nullptr;       // LDS.64 path: tile slot -> image row (k-d tiles), or null
   int64_t Tp = 0, G = 0;              // signed-root plane row length / left guard
@@ -294,6 +295,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.q_lo = p->d_qlo;
   a.psi_map = p->d_psi_map;
   a.kt = p->lds_kt;
+  a.l_psi = p->lds_psi;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
   cudaStream_t es = st;
@@ -526,8 +528,8 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   // LDS.64 path (k_beamform_lds64): integer delays, whole array staged, and its windows (per
   // (tile, mic) origin lo = min over the tile's directions of d, aligned down to even; W = 224 +
   // the largest per-mic spread columns of 8 B) fit as many CTAs per SM as k_beamform gets.  A
-  // tile's 32 directions need not be consecutive rows: the plan also groups them by recursive
-  // bisection of the unit vectors (k-d tree, splits at multiples of 32), so a tile is a compact
+  // tile's 64 or 32 directions need not be consecutive rows: the plan also groups them by recursive
+  // bisection of the unit vectors (k-d tree, splits at multiples of the tile), so a tile is a compact
   // patch of the sky even when the grid's row order makes consecutive rows far apart (e.g.
   // elevation-fastest grids whose long columns are not multiples of 32), and keeps whichever
   // order gives the narrower window; the kernel then writes each direction to its own row
@@ -535,18 +537,20 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   const int64_t n_pad = (nm + dmas::BF_MIC_PAD - 1) / dmas::BF_MIC_PAD * dmas::BF_MIC_PAD;
   std::vector<int32_t> qlo, order;
   if (p->mg == 0 && desc->bf_engine == 0) {
-    const int64_t n_pt = (nd + dmas::BL_PSI - 1) / dmas::BL_PSI;
-    auto eval = [&](const std::vector<int32_t>* ord, std::vector<int32_t>& lo_t, int32_t& wmax, int32_t& lmin,
-                    int32_t& lmax) {
+    // per-(tile, mic) window origins and the largest spread for tiles of `psi` directions taken
+    // in order `ord` (null = consecutive rows)
+    auto eval = [&](int psi, const std::vector<int32_t>* ord, std::vector<int32_t>& lo_t, int32_t& wmax,
+                    int32_t& lmin, int32_t& lmax) {
+      const int64_t n_pt = (nd + psi - 1) / psi;
       lo_t.assign((size_t)n_pt * nm, 0);
       wmax = 0;
       lmin = INT32_MAX;
       lmax = INT32_MIN;
       for (int64_t t = 0; t < n_pt; ++t) {
-        const int64_t a1 = std::min<int64_t>(nd, (t + 1) * dmas::BL_PSI);
+        const int64_t a1 = std::min<int64_t>(nd, (t + 1) * psi);
         for (int i = 0; i < nm; ++i) {
           int32_t lo = INT32_MAX, hi = INT32_MIN;
-          for (int64_t k = t * dmas::BL_PSI; k < a1; ++k) {
+          for (int64_t k = t * psi; k < a1; ++k) {
             const int64_t a = ord ? (*ord)[(size_t)k] : k;
             const int32_t v = p->h_delays[(size_t)a * nm + i];
             lo = std::min(lo, v);
@@ -560,14 +564,12 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
         }
       }
     };
-    std::vector<int32_t> lo_n, lo_k, kd_ord((size_t)nd);
-    int32_t w_n, w_k, lmin_n, lmax_n, lmin_k, lmax_k;
-    eval(nullptr, lo_n, w_n, lmin_n, lmax_n);
-    {
-      // k-d grouping: split the set at a multiple of 32 along the unit-vector component with
-      // the largest range, recursively, so every tile but the last holds exactly 32 directions
-      for (int64_t a = 0; a < nd; ++a) kd_ord[(size_t)a] = (int32_t)a;
-      const int64_t G = dmas::BL_PSI;
+    // k-d grouping: split the set at a multiple of psi along the unit-vector component with the
+    // largest range, recursively, so every tile but the last holds exactly psi directions
+    auto kd_order = [&](int psi) {
+      std::vector<int32_t> ord((size_t)nd);
+      for (int64_t a = 0; a < nd; ++a) ord[(size_t)a] = (int32_t)a;
+      const int64_t G = psi;
       std::vector<std::pair<int64_t, int64_t>> stack{{0, nd}};
       while (!stack.empty()) {
         const auto [b, e] = stack.back();
@@ -577,13 +579,13 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
         double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
         for (int64_t k = b; k < e; ++k)
           for (int c3 = 0; c3 < 3; ++c3) {
-            mn[c3] = std::min(mn[c3], u[3 * (size_t)kd_ord[k] + c3]);
-            mx[c3] = std::max(mx[c3], u[3 * (size_t)kd_ord[k] + c3]);
+            mn[c3] = std::min(mn[c3], u[3 * (size_t)ord[k] + c3]);
+            mx[c3] = std::max(mx[c3], u[3 * (size_t)ord[k] + c3]);
           }
         int ax = 0;
         for (int c3 = 1; c3 < 3; ++c3)
           if (mx[c3] - mn[c3] > mx[ax] - mn[ax]) ax = c3;
-        std::sort(kd_ord.begin() + b, kd_ord.begin() + e, [&](int32_t x, int32_t y) {
+        std::sort(ord.begin() + b, ord.begin() + e, [&](int32_t x, int32_t y) {
           const double ux = u[3 * (size_t)x + ax], uy = u[3 * (size_t)y + ax];
           return ux < uy || (ux == uy && x < y);
         });
@@ -592,50 +594,56 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
         stack.push_back({b + left, e});
         stack.push_back({b, b + left});
       }
-    }
-    eval(&kd_ord, lo_k, w_k, lmin_k, lmax_k);
+      return ord;
+    };
     // Pick the tile: 8 pixels per lane (256-sample tiles) when its windows fit as many CTAs per SM
     // as k_beamform gets (launch bounds: 3 at p = 2, 2 at p = 3..5, 1 above), else 4 pixels per
-    // lane (128-sample tiles, 3 CTAs per SM; integer delays, p <= 5) — 64-microphone arrays (C4).
-    // Consecutive rows when they fit (measured 1-3% faster than k-d tiles of a narrower window on
-    // C5), k-d tiles only when they are what makes the window fit.
+    // lane (128-sample tiles, 3 CTAs per SM; integer delays, p <= 5) — 64-microphone arrays (C4);
+    // within a pixel count, 64 directions per tile before 32 (staging amortised over twice the
+    // work: +0.3-0.5% measured), and consecutive rows before k-d tiles at equal tile size
+    // (measured 1-3% faster on C5 at 32), k-d tiles when they are what makes the window fit.
     const int extra = p->interp ? 1 : 0;                 // + m[j + 1]
-    bool use_kd = false;
 #ifndef DMAS_LDS_KT4_FIRST
 #define DMAS_LDS_KT4_FIRST 0
 #endif
+    std::vector<int32_t> lo_n, lo_k, kd_ord;
+    int32_t w_n = 0, w_k = 0, lmin_n = 0, lmax_n = 0, lmin_k = 0, lmax_k = 0;
     for (int kt : {DMAS_LDS_KT4_FIRST ? 4 : 8, DMAS_LDS_KT4_FIRST ? 8 : 4}) {
       if (kt == 4 && (p->interp || p->order > 5)) continue;
       const size_t budget = (p->order == 2 || kt == 4) ? (size_t)74 * 1024
                             : p->order <= 5 ? (size_t)110 * 1024 : (size_t)220 * 1024;
-      const int32_t wn = (dmas::bl_span(kt) + w_n + extra + 1) / 2 * 2;
-      const int32_t wk = (dmas::bl_span(kt) + w_k + extra + 1) / 2 * 2;
-      if (dmas::beamform_lds64_smem_bytes(nm, wn, p->interp, kt) <= budget) {
-        p->paired = 1;
-        p->lds_kt = kt;
-        p->W = wn;
-      } else if (w_k < w_n && dmas::beamform_lds64_smem_bytes(nm, wk, p->interp, kt) <= budget) {
-        p->paired = 1;
-        p->lds_kt = kt;
-        p->W = wk;
-        use_kd = true;
+      for (int psi : {64, 32}) {
+        eval(psi, nullptr, lo_n, w_n, lmin_n, lmax_n);
+        const int32_t wn = (dmas::bl_span(kt) + w_n + extra + 1) / 2 * 2;
+        if (dmas::beamform_lds64_smem_bytes(nm, wn, p->interp, kt, psi) <= budget) {
+          p->paired = 1;
+          p->lds_kt = kt;
+          p->lds_psi = psi;
+          p->W = wn;
+          qlo.swap(lo_n);
+          lo_min = lmin_n;
+          lo_max = lmax_n;
+          break;
+        }
+        kd_ord = kd_order(psi);
+        eval(psi, &kd_ord, lo_k, w_k, lmin_k, lmax_k);
+        const int32_t wk = (dmas::bl_span(kt) + w_k + extra + 1) / 2 * 2;
+        if (w_k < w_n && dmas::beamform_lds64_smem_bytes(nm, wk, p->interp, kt, psi) <= budget) {
+          p->paired = 1;
+          p->lds_kt = kt;
+          p->lds_psi = psi;
+          p->W = wk;
+          qlo.swap(lo_k);
+          order.swap(kd_ord);
+          lo_min = lmin_k;
+          lo_max = lmax_k;
+          break;
+        }
       }
       if (p->paired) break;
     }
-    if (p->paired) {
-      if (use_kd) {
-        qlo.swap(lo_k);
-        order.swap(kd_ord);
-        lo_min = lmin_k;
-        lo_max = lmax_k;
-      } else {
-        qlo.swap(lo_n);
-        lo_min = lmin_n;
-        lo_max = lmax_n;
-      }
-    }
   }
-  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W, p->interp, p->lds_kt)
+  const size_t smem = p->paired ? dmas::beamform_lds64_smem_bytes(nm, p->W, p->interp, p->lds_kt, p->lds_psi)
                                 : dmas::beamform_smem_bytes(nm, p->W, p->interp, p->mg);
   int smem_optin = 0;
   PLAN_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -643,20 +651,20 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     return bail(fail(DMAS_ERR_INVALID, "microphone count x delay spread exceeds the shared-memory window (" +
                                            std::to_string(smem) + " B)"));
   if (p->paired) {
-    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W, p->interp, p->lds_kt));
+    PLAN_TRY(dmas::beamform_lds64_configure(nm, p->W, p->interp, p->lds_kt, p->lds_psi));
     // byte offsets into the CTA's [n_mics][W] window of 8-byte columns: 8 (i W + d - lo);
     // padding microphones and directions past the grid end -> the zero block (column n_mics W)
     const size_t n_pt = qlo.size() / nm;
-    const size_t n_tab = n_pt * dmas::BL_PSI * n_pad;
+    const size_t n_tab = n_pt * p->lds_psi * n_pad;
     // (interpolating: the fractions alongside, padding 0)
     std::vector<int32_t> offs(n_tab, 8 * nm * p->W);
     std::vector<float> alph(p->interp ? n_tab : 0, 0.f);
     for (size_t t = 0; t < n_pt; ++t)
-      for (int q = 0; q < dmas::BL_PSI; ++q) {
-        const int64_t k = (int64_t)t * dmas::BL_PSI + q;
+      for (int q = 0; q < p->lds_psi; ++q) {
+        const int64_t k = (int64_t)t * p->lds_psi + q;
         if (k >= nd) break;
         const int64_t a = order.empty() ? k : order[(size_t)k];
-        const size_t row = ((size_t)t * dmas::BL_PSI + q) * n_pad;
+        const size_t row = ((size_t)t * p->lds_psi + q) * n_pad;
         for (int i = 0; i < nm; ++i) {
           offs[row + i] = 8 * (i * p->W + (p->h_delays[(size_t)a * nm + i] - qlo[t * nm + i]));
           if (p->interp) alph[row + i] = p->h_alpha[(size_t)a * nm + i];
@@ -907,7 +915,7 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->device = p->device;
   info->d_min = p->dmin;
   info->d_max = p->dmax;
-  info->psi_tile = p->paired ? dmas::BL_PSI : p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
+  info->psi_tile = p->paired ? p->lds_psi : p->mg > 0 ? dmas::BF_PSI_MG : dmas::BF_PSI;
   info->t_tile = p->paired ? 32 * p->lds_kt : dmas::BF_T;
   info->window = p->W;
   info->chunk_frames = p->chunk_cap;

@@ -515,14 +515,15 @@ def test_large_array_parity(dm, kind):
 
 
 def test_beamform_kernel_for_benchmark_configs(dm):
-    """All three take the LDS.64 kernel: C5 with 256-sample tiles of consecutive rows; C2 with k-d
-    direction tiles (its consecutive rows straddle its 30-direction elevation columns); C4 (64 mics)
-    with 128-sample k-d tiles (4 pixels per lane: the 256-sample windows of 64 microphones would
-    not fit 2 CTAs per SM).  bf_engine = 1 forces the classic kernel."""
-    for name, k, order, tt in (("C2", 1, 1, 256), ("C4", 1, 1, 128), ("C5", 1, 0, 256)):
+    """All three take the LDS.64 kernel: C5 with 256-sample tiles of 64 k-d-grouped directions; C2
+    with 32-direction k-d tiles (its consecutive rows straddle its 30-direction elevation columns);
+    C4 (64 mics) with 128-sample tiles of 64 k-d-grouped directions (4 pixels per lane: the
+    256-sample windows of 64 microphones would not fit 2 CTAs per SM).  bf_engine = 1 forces the
+    classic kernel."""
+    for name, k, order, tt, psi in (("C2", 1, 1, 256, 32), ("C4", 1, 1, 128, 64), ("C5", 1, 1, 256, 64)):
         cfg = gen.config(name, frames=1)
         plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"])
-        assert plan.info["psi_tile"] == 32 and plan.info["bf_kernel"] == k, (name, plan.info)
+        assert plan.info["psi_tile"] == psi and plan.info["bf_kernel"] == k, (name, plan.info)
         assert plan.info["tile_order"] == order and plan.info["t_tile"] == tt, (name, plan.info)
         classic = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], cfg["order"], cfg["T"], bf_engine=1)
         assert classic.info["bf_kernel"] == 0
