@@ -531,7 +531,8 @@ def test_beamform_kernel_for_benchmark_configs(dm):
 
 # ------------------------------------------------------------------ LDS.64 kernel (k_beamform_lds64)
 @pytest.mark.parametrize("case", ["C5p2", "C5p3", "C5p4", "C5p5", "C2p2", "C4p3", "C4p5", "ragged", "ragged_p6", "tiny",
-                                  "short_T", "scattered", "C5p2i", "C5p3i", "C5p5i", "C2p2i", "ragged_i"])
+                                  "short_T", "scattered", "kt4_ragged", "C5p2i", "C5p3i", "C5p5i", "C2p2i",
+                                  "ragged_i"])
 def test_lds64_kernel_bitwise_and_parity(dm, case):
     """k_beamform_lds64 (paired root plane, one LDS.64 per 2 pixels, pixel-pair packed FP32)
     performs the same per-pixel operations in the same microphone order as the classic kernel:
@@ -549,6 +550,10 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
     elif case.startswith("C4"):                             # 64 mics: 4 pixels per lane, k-d tiles
         cfg = gen.config("C4", frames=1)
         p, mic, dirs, sig = int(case[-1]), cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"]
+    elif case == "kt4_ragged":                               # 64 mics: 4 pixels per lane, T = 301
+        p, mic = 2, gen.disk_array(64, 0.10, 4e-3, seed=11)   # (2 full 128-sample tiles + 45),
+        dirs = gen.az_el_grid(10, 20.0, 10, 10.0)             # 100 directions (3 full 32-tiles + 4)
+        sig = gen.random_signals(2, 64, 301, seed=67, sparsity=0.1)
     elif case == "scattered":                                # 500 random directions in random order:
         cfg = gen.config("C5", frames=1)                      # only k-d tiles can fit the window
         rng = np.random.default_rng(66)
@@ -576,6 +581,8 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
         assert plan.info["bf_kernel"] == (1 if eng == 0 else 0), plan.info
         if case == "scattered" and eng == 0:
             assert plan.info["tile_order"] == 1, plan.info
+        if case == "kt4_ragged" and eng == 0:
+            assert plan.info["t_tile"] == 128, plan.info
         r = plan.beamform(x, what)
         torch.cuda.synchronize()
         res.append({k: v.cpu().numpy() for k, v in r.items()})
