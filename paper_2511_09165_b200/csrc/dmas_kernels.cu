@@ -905,6 +905,34 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   mbar_wait(&bar, 0);
 
   const uint32_t la = smem_u32(win) + 8u * (uint32_t)lane;
+  if constexpr (KM == 1 && !INTERP) {
+    // DAS-only request (Eq. (2)): the prologue wrote the identity plane (x = m, no
+    // roots), so the sum over microphones is one packed FADD2 per pixel pair and LDS.64
+    for (int q = warp; q < npsi; q += BF_WARPS) {
+      float2 acc[KT / 2];
+#pragma unroll
+      for (int m = 0; m < KT / 2; ++m) acc[m] = f2(0.f, 0.f);
+      const int4* o4 = reinterpret_cast<const int4*>(offs + q * n_pad);
+#pragma unroll 1
+      for (int j = 0; j < n_pad / 4; j += 2) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int4 o = o4[j + u];
+          const int oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int m = 0; m < KT / 2; ++m) acc[m] = __fadd2_rn(acc[m], lds_f32x2(la + (uint32_t)oo[h] + 512u * m));
+        }
+      }
+      const int64_t psi = a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q;
+      const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
+#pragma unroll
+      for (int k = 0; k < KT; ++k)
+        if (t0 + lane + 32 * k < a.T) a.out[0][o + 32 * k] = (k & 1) ? acc[k >> 1].y : acc[k >> 1].x;
+    }
+    return;
+  }
   constexpr int U = bf_unroll<P>();
   for (int q = warp; q < npsi; q += BF_WARPS) {
     PAcc<P> acc[KT / 2];
@@ -992,6 +1020,9 @@ static cudaError_t configure_order_lds64(int bytes) {
 cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi) {
   const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp, kt, psi);
   cudaError_t e;
+  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<2, 1, false, 8>, attr, bytes))) return e;   // DAS-only
+  if ((e = cudaFuncSetAttribute(k_beamform_lds64<2, 1, false, 4>, attr, bytes))) return e;
   if ((e = configure_order_lds64<2>(bytes))) return e;
   if ((e = configure_order_lds64<3>(bytes))) return e;
   if ((e = configure_order_lds64<4>(bytes))) return e;
@@ -1016,8 +1047,12 @@ cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t m
 template <int P>
 static void launch_order(const BeamformArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   const bool only_cfdmas = !a.out[0] && !a.out[1] && a.out[2] && !a.out[3] && !a.out[4];
+  const bool only_das = a.out[0] && !a.out[1] && !a.out[2] && !a.out[3] && !a.out[4];
   if (a.q_lo) {                                        // paired plane, LDS.64 gathers
-    if (a.alpha) {
+    if (only_das && !a.alpha) {                        // identity plane (dmas_plan.cpp enqueue_chunk)
+      if (a.kt == 4) k_beamform_lds64<2, 1, false, 4><<<grid, BF_THREADS, smem, st>>>(a);
+      else k_beamform_lds64<2, 1, false, 8><<<grid, BF_THREADS, smem, st>>>(a);
+    } else if (a.alpha) {
       if (only_cfdmas) k_beamform_lds64<P, 4, true, 8><<<grid, BF_THREADS, smem, st>>>(a);
       else k_beamform_lds64<P, 31, true, 8><<<grid, BF_THREADS, smem, st>>>(a);
     } else if (a.kt == 4) {

@@ -264,14 +264,18 @@ dmas_status validate(const dmas_plan_desc* d) {
 // already point at the chunk's first frame.
 dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* const* raw_dst,
                           float* const* env_dst, uint32_t env_kinds, cudaStream_t st) {
+  // DAS-only requests on the LDS.64 path sum the samples themselves: identity plane (order 1), no
+  // roots (the kernel selects its DAS-only variant on the same condition, dmas_kernels.cu)
+  const bool das_only = raw_dst[0] && !raw_dst[1] && !raw_dst[2] && !raw_dst[3] && !raw_dst[4];
+  const int root_order = (p->interp || (das_only && p->paired)) ? 1 : p->order;
   if (p->mf_taps > 0) {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
-      return dmas::launch_mf_roots(p->interp ? 1 : p->order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
+      return dmas::launch_mf_roots(root_order, sig, p->T_in, p->d_mf, p->mf_lp, p->mf_inv_energy, p->d_splane,
                                    (int64_t)nf * p->n_mics, p->T, p->Tp, p->G, p->paired, st);
     }));
   } else {
     CUDA_TRY(timed(p, K_ROOTS, st, [&] {
-      return dmas::launch_signed_roots(p->interp ? 1 : p->order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T,
+      return dmas::launch_signed_roots(root_order, sig, p->d_splane, (int64_t)nf * p->n_mics, p->T,
                                        p->Tp, p->G, p->paired, st);
     }));
   }

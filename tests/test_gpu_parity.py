@@ -603,3 +603,46 @@ def test_lds64_kernel_bitwise_and_parity(dm, case):
     scale = math.comb(len(mic), p) * float(np.max(np.abs(sig))) + len(mic) * float(np.max(np.abs(sig)))
     for key in ref:
         assert_parity(res[0][key], ref[key], f"lds64 {case} {key}", zero_scale=scale)
+
+
+@pytest.mark.parametrize("case", ["C5", "kt4", "ragged", "raw_mf"])
+def test_das_only_identity_plane(dm, case):
+    """A DAS-only request (raw and/or envelope) on the LDS.64 path sums the samples themselves
+    (identity plane, one FADD2 per pixel pair) instead of rebuilding x from the signed roots:
+    within the oracle bar, and within fp32 rounding of the DAS an all-kinds request returns."""
+    import torch
+    kw = {}
+    if case == "C5":
+        cfg = gen.config("C5", frames=2)
+        mic, dirs, sig, T = cfg["mic_xyz"], cfg["dirs"][:300], cfg["signals"], cfg["T"]
+    elif case == "kt4":
+        mic, dirs = gen.disk_array(64, 0.10, 4e-3, seed=11), gen.az_el_grid(10, 20.0, 10, 10.0)
+        sig = gen.random_signals(2, 64, 301, seed=68, sparsity=0.1)
+        T = 301
+    elif case == "ragged":
+        mic, dirs = gen.disk_array(13, 0.09, 5e-3, seed=61), gen.az_el_grid(23, 85.0, 7, 55.0)
+        sig = gen.random_signals(2, 13, 601, seed=69, sparsity=0.2)
+        T = 601
+    else:
+        cfg = gen.raw_config("C1", frames=2)
+        mic, dirs, T = cfg["mic_xyz"], cfg["dirs"], cfg["T"]
+        kw["mf_coeffs"] = cfg["chirp"]
+        sig = cfg["signals"]
+    plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, 3, T, max_frames=sig.shape[0], **kw)
+    assert plan.info["bf_kernel"] == 1, plan.info
+    x = torch.from_numpy(np.ascontiguousarray(sig)).cuda()
+    das = plan.beamform(x, dm.RAW(dm.KIND_DAS) | dm.ENV(dm.KIND_DAS))
+    env_only = plan.beamform(x, dm.ENV(dm.KIND_DAS))[("env", "das")].cpu().numpy()
+    full = plan.beamform(x, what_all(dm))
+    torch.cuda.synchronize()
+    g_raw, g_env = das[("raw", "das")].cpu().numpy(), das[("env", "das")].cpu().numpy()
+    assert np.array_equal(g_env, env_only)
+    m = O.matched_filter(sig, cfg["chirp"], T) if case == "raw_mf" else sig
+    d = O.delay_table(mic, dirs, gen.FS, gen.C_SOUND)
+    h = O.lpf_taps()
+    for f in range(sig.shape[0]):
+        ref = O.beamform_frame(m[f], d, 3)["das"]
+        assert_parity(g_raw[f][None], ref[None], f"das-only {case} raw f{f}")
+        assert_parity(g_env[f][None], O.envelope(ref, h)[None], f"das-only {case} env f{f}")
+        fr = full[("raw", "das")][f].cpu().numpy()
+        assert np.max(np.abs(fr - g_raw[f])) <= 1e-5 * np.max(np.abs(fr))
