@@ -21,9 +21,12 @@
  *  - Validation errors are returned synchronously, before any device work is enqueued.
  *    Asynchronous device faults surface as DMAS_ERR_CUDA at a later call or stream sync.
  *  - Device pointers must belong to the plan's device and be 4-byte aligned.
- *  - A plan is immutable after dmas_plan() (except its internal scratch); it may be used
- *    by one in-flight dmas_beamform* call at a time (calls on one plan are serialised by
- *    an internal mutex).  Distinct plans are independent.
+ *  - A plan is immutable after dmas_plan() (except its internal scratch, which dmas_plan
+ *    allocates: a call never allocates device memory or synchronises).  Host-side, calls on
+ *    one plan are serialised by an internal mutex; device-side, the work a call enqueues is
+ *    ordered after the previous call's work on the same plan (a plan-owned event the new
+ *    call's stream waits on), whatever streams the two calls use, because both use the
+ *    plan's signed-root plane and scratch.  Distinct plans are independent.
  */
 #ifndef DMAS_H
 #define DMAS_H
@@ -88,7 +91,7 @@ typedef struct {
   const float* bp_coeffs;    /* [bp_taps] host, copied; applied before |.| as a centred FIR      */
   int32_t env_decim;         /* R >= 1: envelope keeps samples t = 0, R, 2R, ... (ceil(T/R))     */
   int32_t env_engine;        /* 0 = auto: tensor-core (tcgen05) low-pass with a 3-pass BF16 split
-                                (error <= ~1.1e-5 of the envelope) when lp_taps <= 127, no
+                                (error <= ~4.6e-5 of the envelope) when lp_taps <= 127, no
                                 band-pass, R == 1, T % 32 == 0 and 16-byte aligned buffers,
                                 else the FP32 FIR; 1 = always the FP32 FIR                      */
   /* Optional matched filter (pulse compression; NEXT-1).  When mf_taps > 0 the
@@ -106,7 +109,9 @@ typedef struct {
   /* Runtime. */
   int32_t device;            /* CUDA device ordinal; -1 = current device                        */
   int64_t scratch_bytes;     /* budget for the plan-owned raw-image scratch used when an
-                                envelope is requested without its raw image; 0 = 4 GiB         */
+                                envelope is requested without its raw image; 0 = 4 GiB.  dmas_plan
+                                allocates min(budget, max_frames frames of all 5 kinds), at least
+                                one frame of every kind (plans with lp_taps > 0 only)           */
   int32_t bf_engine;         /* beamform kernel: 0 = auto (the LDS.64 kernel -- paired root plane,
                                 one 8-byte shared load per 2 pixels -- when delays are integer and
                                 its windows fit two CTAs per SM, else the classic one); 1 = always

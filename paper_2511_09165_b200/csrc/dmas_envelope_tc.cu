@@ -9,9 +9,12 @@
 // i.e. per 128-block tile five M=128 x N=32 x K=32 GEMMs.  MACs per output = 160 (127 useful).
 //
 // Precision: 3-pass BF16 split a = a_hi + a_lo, h = h_hi + h_lo; hi*hi + hi*lo + lo*hi with fp32
-// accumulation in TMEM.  Relative error per product <= 2^-18 + 2^-17 ~ 1.1e-5; all but 34 tiny
-// taps are positive, so the summed error is <= ~1.1e-5 of the envelope value itself (9x inside
-// the 1e-4 parity bar).
+// accumulation in TMEM.  BF16 keeps 8 significant bits, so |a - a_hi| <= 2^-8 |a| and the rounded
+// lo part leaves <= 2^-16 |a| (same for h); with the dropped lo*lo term (<= 2^-16) the relative
+// error per product is <= ~3 * 2^-16 ~ 4.6e-5.  The rectified input is >= 0 and all but 34 tiny
+// taps are positive, so the summed error is <= ~4.6e-5 of the envelope value itself: about 2x
+// inside the 1e-4 parity bar in the worst case (measured: ~2e-6 on C1-C5 images; the adversarial
+// rows of tests/test_gpu_parity.py::test_envelope_tc_adversarial_split_inputs).
 //
 // Why this shape (measured on B200, round-1 microbenchmarks): every tcgen05.mma with N <= 64
 // costs >= 44 cycles, and in SS mode the 4 KB A operand was re-read from shared memory by every
@@ -212,7 +215,7 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 // BF16 hi / lo split of two non-negative values with integer rounding (round half up on the
-// magnitude; |a - hi| <= 2^-9 |a|, lo = a - hi exact, |lo - bf16(lo)| <= 2^-9 |lo|), packed as bf16x2
+// magnitude; |a - hi| <= 2^-8 |a|, lo = a - hi exact, |lo - bf16(lo)| <= 2^-8 |lo|), packed as bf16x2
 // (first value in the low half).  ALU + FADD only: no F2F on the MIO pipe.
 __device__ __forceinline__ void split2(float a0, float a1, uint32_t& hi2, uint32_t& lo2) {
   const uint32_t h0 = (__float_as_uint(a0) + 0x8000u) & 0xFFFF0000u;

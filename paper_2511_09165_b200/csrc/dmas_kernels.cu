@@ -8,8 +8,9 @@
 //                     Newton-Girard and CF, fused.
 // K4 k_envelope_*   — A5 |.| + low-pass, optional band-pass, clamp, decimate.
 //
-// Design notes: the path is a gather-plus-reduction, so no tensor cores.
-// K3 is bound by the FP32 pipe (5 FP32 ops per mic-pixel at p = 2) with shared-memory bandwidth
+// Design notes: A2-A4 are a gather-plus-reduction, so K1-K3 use no tensor
+// cores; the one dense contraction, K4's low-pass, runs on tcgen05 (dmas_envelope_tc.cu) unless
+// the plan asks for the FP32 FIR (env_engine = 1).  K3 is bound by the FP32 pipe (5 FP32 ops per mic-pixel at p = 2) with shared-memory bandwidth
 // close behind; its staging is one cp.async.bulk (TMA bulk engine) per microphone row into a
 // window reused by BF_PSI directions; packed FADD2/FFMA2 halve the issue slots of the accumulate.
 
@@ -709,7 +710,9 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_beamform_mg(const BeamformArg
 // ------------------------------------------------------------------------------------------
 // K3p — k_beamform_lds64 (integer delays, whole array staged): same tile (BF_PSI directions x
 // BF_T samples, one direction per warp at a time, lane pixels t0 + lane + 32k, k < 8), same
-// per-pixel arithmetic, microphone order and epilogue as k_beamform (bit-identical images), but
+// per-pixel arithmetic, microphone order and epilogue as k_beamform (bit-identical images for
+// every request that includes a root-based kind; a DAS-only request sums the samples themselves
+// on the identity plane and is then more exact, not bitwise equal to k_beamform's DAS), but
 // a lane fetches the samples of its pixels k and k + 1 with ONE LDS.64 from the paired plane
 // (column j = (S[j], S[j + 32])): the word for direction psi and mic i is column
 // t0 + lane + 64 m + d(psi, i), 8-byte aligned for any delay, lanes on consecutive columns

@@ -111,11 +111,17 @@ struct dmas_plan_s {
   size_t scratch_cap = 0;
   int64_t scratch_budget = 0;
 
-  // host pipeline buffers (dmas_beamform_host)
+  // host pipeline buffers (dmas_beamform_host), created on first use and kept
   cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
   float* d_hsig[2] = {nullptr, nullptr};
   float* d_hout[2] = {nullptr, nullptr};
   size_t hsig_cap = 0, hout_cap = 0;
+  cudaEvent_t h_ev[3][2] = {};                       // h2d_done, comp_done, d2h_done per buffer
+
+  // cross-stream ordering: every call's work waits for the previous call's (the signed-root plane
+  // and the scratch are shared by all calls on this plan), whatever stream either was issued on
+  cudaEvent_t ev_last = nullptr;
+  bool ev_last_recorded = false;
 
   // timing
   bool timing = false;
@@ -173,6 +179,10 @@ void free_plan_memory(dmas_plan_s* p) {
   }
   for (auto& s : p->hs)
     if (s) cudaStreamDestroy(s);
+  for (auto& row : p->h_ev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+  if (p->ev_last) cudaEventDestroy(p->ev_last);
 
   for (auto& r : p->recs) {
     cudaEventDestroy(r.ev0);
@@ -349,24 +359,18 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     if (!outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
     if (((uintptr_t)outs[i]) & 3u) return fail(DMAS_ERR_SHAPE, "misaligned output pointer");
   }
-  // envelope kinds without their raw image go through the plan's scratch
+  // envelope kinds without their raw image go through the plan's scratch (allocated by dmas_plan:
+  // at least one frame of every kind, so a call never allocates or synchronises)
   const uint32_t env_only = env_k & ~raw_k;
   const int n_scratch = popcount5(env_only);
   const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
   int32_t chunk = std::min(p->chunk_cap, n_frames);
   if (n_scratch > 0) {
-    const int64_t fit = p->scratch_budget / (int64_t)(frame_img * n_scratch);
-    chunk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(chunk, fit));
-    const size_t need = (size_t)chunk * n_scratch * frame_img;
-    if (need > p->scratch_cap) {
-      CUDA_TRY(cudaStreamSynchronize(st));
-      cudaFree(p->d_scratch);
-      p->d_scratch = nullptr;
-      p->scratch_cap = 0;
-      CUDA_TRY(cudaMalloc(&p->d_scratch, need));
-      p->scratch_cap = need;
-    }
+    const size_t fit = p->scratch_cap / (frame_img * n_scratch);
+    if (fit < 1) return fail(DMAS_ERR_CUDA, "internal: envelope scratch smaller than one frame");
+    chunk = (int32_t)std::min<size_t>((size_t)chunk, fit);
   }
+  if (p->ev_last_recorded) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_last, 0));
   for (int32_t f0 = 0; f0 < n_frames; f0 += chunk) {
     const int32_t nf = std::min(chunk, n_frames - f0);
     float* raw_dst[dmas::N_KINDS] = {};
@@ -381,6 +385,8 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st);
     if (rc != DMAS_OK) return rc;
   }
+  CUDA_TRY(cudaEventRecord(p->ev_last, st));
+  p->ev_last_recorded = true;
   return DMAS_OK;
 }
 
@@ -783,7 +789,16 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       for (int i = 0; i < p->lp_taps; ++i) p->lp127.h[i] = p->h_lp[i];
     if (p->lp_tc) PLAN_TRY(dmas::envelope_tc_configure());
     PLAN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    // raw-image scratch for envelope-only kinds: the budget (default 4 GiB), capped at what
+    // max_frames frames of all five kinds need, and never below one frame of every kind
+    const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
+    const size_t all_kinds = frame_img * dmas::N_KINDS;
+    size_t cap = std::min<size_t>((size_t)p->scratch_budget, all_kinds * (size_t)p->max_frames);
+    cap = std::max(cap, all_kinds);
+    PLAN_TRY(cudaMalloc(&p->d_scratch, cap));
+    p->scratch_cap = cap;
   }
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming));
   PLAN_TRY(cudaDeviceSynchronize());
 #undef PLAN_TRY
   *out = p;
@@ -849,12 +864,12 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
     p->hsig_cap = sig_frame * hc;
     p->hout_cap = out_frame_total * hc;
   }
-  cudaEvent_t h2d_done[2], comp_done[2], d2h_done[2];
-  for (int b = 0; b < 2; ++b) {
-    CUDA_TRY(cudaEventCreateWithFlags(&h2d_done[b], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&comp_done[b], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&d2h_done[b], cudaEventDisableTiming));
-  }
+  for (auto& row : p->h_ev)
+    for (auto& e : row)
+      if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t* h2d_done = p->h_ev[0];
+  cudaEvent_t* comp_done = p->h_ev[1];
+  cudaEvent_t* d2h_done = p->h_ev[2];
   dmas_status rc = DMAS_OK;
   int chunk_idx = 0;
   for (int32_t f0 = 0; f0 < n_frames && rc == DMAS_OK; f0 += hc, ++chunk_idx) {
@@ -884,11 +899,6 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
   cudaError_t e = cudaStreamSynchronize(p->hs[2]);
   cudaStreamSynchronize(p->hs[1]);
   cudaStreamSynchronize(p->hs[0]);
-  for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(h2d_done[b]);
-    cudaEventDestroy(comp_done[b]);
-    cudaEventDestroy(d2h_done[b]);
-  }
   if (rc != DMAS_OK) return rc;
   if (e != cudaSuccess) return fail(DMAS_ERR_CUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
   return DMAS_OK;

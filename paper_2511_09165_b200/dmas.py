@@ -140,9 +140,9 @@ def _f64(a, shape_last):
     return a
 
 
-def _current_stream_ptr():
+def _current_stream_ptr(device: int):
     import torch
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class Plan:
@@ -225,18 +225,22 @@ class Plan:
         n_in = self.n_samples + max(0, self.mf_taps - 1)
         if not signals.is_contiguous() or signals.dim() != 3 or signals.shape[1:] != (self.n_mics, n_in):
             raise ValueError(f"signals must be contiguous [F][{self.n_mics}][{n_in}], got {tuple(signals.shape)}")
+        if signals.device.index != self.device:
+            raise ValueError(f"signals are on cuda:{signals.device.index}, the plan on cuda:{self.device}")
         F = signals.shape[0]
         shapes = self.out_shapes(F, what)
         if outs is None:
             outs = [torch.empty(s, dtype=torch.float32, device=signals.device) for (_, _, s) in shapes]
         if len(outs) != len(shapes):
-            raise ValueError("wrong number of output buffers")
+            raise ValueError(f"{len(outs)} output buffers for {len(shapes)} requested outputs")
         for o, (_, _, s) in zip(outs, shapes):
             if tuple(o.shape) != s or o.dtype != torch.float32 or not o.is_contiguous() or not o.is_cuda:
                 raise ValueError(f"output buffer must be contiguous float32 {s}")
+            if o.device.index != self.device:
+                raise ValueError(f"output buffer on cuda:{o.device.index}, the plan on cuda:{self.device}")
         arr = (ctypes.c_void_p * max(1, len(outs)))(*[o.data_ptr() for o in outs])
         st = ctypes.c_void_p(stream) if isinstance(stream, int) else (
-            ctypes.c_void_p(stream.cuda_stream) if stream is not None else _current_stream_ptr())
+            ctypes.c_void_p(stream.cuda_stream) if stream is not None else _current_stream_ptr(self.device))
         _check(lib.dmas_beamform(self._h, ctypes.c_void_p(signals.data_ptr()), F, arr, what, st))
         return {(stage, name): o for (stage, name, _), o in zip(shapes, outs)}
 
@@ -250,6 +254,8 @@ class Plan:
         shapes = self.out_shapes(F, what)
         if outs is None:
             outs = [np.empty(s, dtype=np.float32) for (_, _, s) in shapes]
+        if len(outs) != len(shapes):
+            raise ValueError(f"{len(outs)} output buffers for {len(shapes)} requested outputs")
         for o, (_, _, s) in zip(outs, shapes):
             if o.shape != s or o.dtype != np.float32 or not o.flags.c_contiguous:
                 raise ValueError(f"output buffer must be contiguous float32 {s}")

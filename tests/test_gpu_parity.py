@@ -184,42 +184,61 @@ def test_config_C3_order_sweep(dm, p):
     _config_parity(dm, "C3", p=p)
 
 
-def _sampled_rows(dm, cfg, p, what, frames_idx, n_rows, seed, **kw):
-    """Full-size GPU run; oracle on sampled (frame, direction) rows (rows are independent)."""
+def _assert_whole_frames(res, label):
+    """res from tests/_oracle_pool.compare_frames: the north_star bar over every pixel of each frame."""
+    assert res
+    for (stage, kind, f), (err, peak, finite) in sorted(res.items()):
+        assert finite, (label, stage, kind, f)
+        assert peak > 0, (label, stage, kind, f)
+        assert err <= TOL * peak, f"{label} {stage}/{kind} frame {f}: max err {err:.3e} > {TOL * peak:.3e}"
+
+
+def test_config_C4_whole_frame_all_kinds(dm):
+    """C4 (64 mics, 16,384 directions, T = 8192, p = 3) frame 0, EVERY kind raw and envelope, over the
+    whole frame (134 M pixels per image) against the oracle (process pool over direction chunks)."""
     import torch
+    from _oracle_pool import compare_frames
+    cfg = gen.config("C4", frames=1)
     sig = cfg["signals"]
-    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, cfg["T"], max_frames=sig.shape[0], **kw)
-    x = torch.from_numpy(sig).cuda()
-    res = plan.beamform(x, what)
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 3, cfg["T"], max_frames=1)
+    res = plan.beamform(torch.from_numpy(sig).cuda(), what_all(dm))
     torch.cuda.synchronize()
+    gpu = {k: v.cpu().numpy() for k, v in res.items()}
+    del res
     d = plan.delay_table()
     assert np.array_equal(d, O.delay_table(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"]))
-    rng = np.random.default_rng(seed)
-    rows = np.sort(rng.choice(len(cfg["dirs"]), n_rows, replace=False))
-    env_k = [k for k in KINDS if (what >> 8) & dm.KIND_BITS[k]]
-    raw_k = [k for k in KINDS if what & dm.KIND_BITS[k]]
-    h = O.lpf_taps()
-    for f in frames_idx:
-        img = O.beamform_frame(sig[f], d[rows], p)
-        for k in raw_k:
-            assert_parity(res[("raw", k)][f][rows].cpu().numpy()[None], img[k][None], f"{cfg['name']} raw {k} f{f}")
-        for k in env_k:
-            assert_parity(res[("env", k)][f][rows].cpu().numpy()[None], O.envelope(img[k], h)[None],
-                          f"{cfg['name']} env {k} f{f}")
-    return res
+    _assert_whole_frames(compare_frames(sig, d, 3, gpu, [0], chunk=128), "C4")
 
 
-def test_config_C4_sampled(dm):
-    cfg = gen.config("C4")
-    _sampled_rows(dm, cfg, 3, dm.RAW(dm.KIND_DAS | dm.KIND_DMAS | dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS),
-                  [0], 96, seed=1)
-
-
-def test_config_C5_bench_launch_sampled(dm):
-    """C5 in the launch configuration bench.py times (256 frames, CF-DMAS2 envelope only,
-    internal frame chunks through the plan scratch); sampled frames {0, 128, 255}."""
+def test_config_C5_bench_launch_whole_frames(dm):
+    """C5 in the launch configuration bench.py times: one call over 256 frames, CF-DMAS2 envelope
+    only (the raw image goes through the plan scratch in internal frame chunks).  Frames
+    {0, 128, 255} are compared over the WHOLE frame (67 M pixels) with the oracle; then the same three
+    frames are beamformed with the raw CF-DMAS image requested too: raw parity over the whole frame,
+    and the envelope of that request is bitwise the bench launch's."""
+    import torch
+    from _oracle_pool import compare_frames
     cfg = gen.config("C5")
-    _sampled_rows(dm, cfg, 2, dm.ENV(dm.KIND_CFDMAS), [0, 128, 255], 48, seed=2)
+    sig = cfg["signals"]
+    frames = [0, 128, 255]
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=sig.shape[0],
+                   lp_taps=127)
+    out = torch.empty((sig.shape[0], len(cfg["dirs"]), cfg["T"]), dtype=torch.float32, device="cuda")
+    plan.beamform(torch.from_numpy(sig).cuda(), dm.ENV(dm.KIND_CFDMAS), outs=[out])
+    torch.cuda.synchronize()
+    env_bench = np.stack([out[f].cpu().numpy() for f in frames])
+    del out
+    r = plan.beamform(torch.from_numpy(np.ascontiguousarray(sig[frames])).cuda(),
+                      dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS))
+    torch.cuda.synchronize()
+    raw = r[("raw", "cfdmas")].cpu().numpy()
+    assert np.array_equal(r[("env", "cfdmas")].cpu().numpy(), env_bench)
+    del r
+    d = plan.delay_table()
+    assert np.array_equal(d, O.delay_table(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"]))
+    res = compare_frames(sig, d, 2, {("raw", "cfdmas"): raw, ("env", "cfdmas"): env_bench}, frames)
+    assert len(res) == 6
+    _assert_whole_frames(res, "C5")
 
 
 # ------------------------------------------------------------------ edge cases and variants
@@ -263,16 +282,22 @@ def test_short_frames_mostly_out_of_range(dm):
 
 
 def test_generic_envelope_bandpass_decimation(dm):
-    """Generic K4 path: 63-tap low-pass at 8 kHz, a 31-tap band-pass, decimation R = 3."""
+    """Generic K4 path: 63-tap low-pass at 8 kHz, a 31-tap band-pass, decimation R = 3; and
+    asymmetric band-pass taps (a linear-phase filter tilted by a ramp, and the one-sample delay
+    [0, 0, 1]) so that the convolution orientation is fixed on the GPU too."""
     import scipy.signal as ss
     bp = ss.firwin(31, [20e3, 60e3], pass_zero=False, fs=gen.FS).astype(np.float32)
+    bp_tilt = (bp * np.linspace(0.3, 1.7, 31)).astype(np.float32)
+    delay1 = np.array([0.0, 0.0, 1.0], dtype=np.float32)
     mic = gen.disk_array(16, seed=5)
     dirs = gen.az_el_grid(5, 60.0, 8, 30.0)
     sig = gen.random_signals(2, 16, 1000, seed=52)
     for kw, okw in [(dict(lp_taps=63, lp_cutoff_hz=8000.0, env_decim=3, bp_coeffs=bp),
                      dict(lp_taps=63, cutoff=8000.0, decim=3, bp=bp.astype(np.float64))),
                     (dict(env_decim=4), dict(decim=4)),
-                    (dict(bp_coeffs=bp), dict(bp=bp.astype(np.float64)))]:
+                    (dict(bp_coeffs=bp), dict(bp=bp.astype(np.float64))),
+                    (dict(bp_coeffs=bp_tilt, env_decim=2), dict(bp=bp_tilt.astype(np.float64), decim=2)),
+                    (dict(bp_coeffs=delay1, lp_taps=1), dict(bp=delay1.astype(np.float64), lp_taps=1))]:
         plan, g = run_gpu(dm, mic, dirs, gen.FS, gen.C_SOUND, 2, sig, dm.ENV(dm.KIND_DAS | dm.KIND_CFDMAS), **kw)
         ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, 2, sig, kinds=(), env_kinds=("das", "cfdmas"), **okw)
         for key in ref:
@@ -357,6 +382,46 @@ def test_envelope_engines(dm, engine, T, L):
                         lp_taps=L)
     for key in ref:
         assert_parity(g[key], ref[key], f"engine={engine} T={T} L={L} {key}")
+
+
+def test_envelope_tc_adversarial_split_inputs(dm):
+    """The tensor-core envelope's 3-pass BF16 split near its worst case: |y| just below a BF16
+    rounding boundary (2^e (1 + 2^-8 - 2^-20): the hi part drops ~2^-8 of the value and the lo part
+    carries it), constant rows (every product's error has the same sign), alternating-sign rows
+    (|.| must see them as constant), impulses that land on the 34 negative taps, and a wide
+    exponent range.  The envelope input is made exact through the slice harness: a 2-microphone
+    array at broadside whose second microphone is silent, so DAS = m_0 exactly."""
+    import torch
+    rng = np.random.default_rng(71)
+    T = 4096
+    rows = []
+    v = 1.0 + 2.0 ** -8 - 2.0 ** -20
+    rows.append(np.full(T, v))                                         # constant, worst hi rounding
+    rows.append(np.where(np.arange(T) % 2 == 0, v, -v))                # alternating sign
+    e = rng.integers(-6, 7, T).astype(np.float64)
+    rows.append(np.sign(rng.standard_normal(T)) * np.exp2(e) * v)      # wide exponent range
+    imp = np.zeros(T)
+    imp[rng.choice(T, 40, replace=False)] = np.exp2(rng.integers(-3, 4, 40)) * v
+    rows.append(imp)                                                   # impulses (negative taps)
+    steps = np.repeat(np.exp2(rng.integers(-4, 5, T // 64)).astype(np.float64), 64) * v
+    rows.append(steps)                                                 # piecewise-constant steps
+    sig = np.zeros((len(rows), 2, T), dtype=np.float32)
+    sig[:, 0, :] = np.stack(rows).astype(np.float32)
+    mic = np.array([[0.0, -0.0015, 0.0], [0.0, 0.0015, 0.0]])
+    plan = dm.Plan(mic, [[0.0, 0.0]], gen.FS, gen.C_SOUND, 2, T, max_frames=len(rows))
+    res = plan.beamform(torch.from_numpy(sig).cuda(), dm.ENV(dm.KIND_DAS) | dm.RAW(dm.KIND_DAS))
+    torch.cuda.synchronize()
+    raw = res[("raw", "das")].cpu().numpy()
+    assert np.array_equal(raw[:, 0, :], sig[:, 0, :])                 # the envelope input is exact
+    env = res[("env", "das")].cpu().numpy()
+    h = O.lpf_taps()
+    worst = 0.0
+    for f in range(len(rows)):
+        ref = O.envelope(sig[f, 0, :].astype(np.float64)[None], h)
+        err = float(np.max(np.abs(env[f] - ref))) / float(np.max(np.abs(ref)))
+        worst = max(worst, err)
+        assert_parity(env[f][None], ref[None], f"adversarial envelope row {f}")
+    print(f"adversarial envelope worst error {worst:.2e} of peak")
 
 
 # ------------------------------------------------------------------ NEXT-1: matched filter on the GPU
@@ -630,6 +695,8 @@ def test_das_only_identity_plane(dm, case):
         sig = cfg["signals"]
     plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, 3, T, max_frames=sig.shape[0], **kw)
     assert plan.info["bf_kernel"] == 1, plan.info
+    if case == "kt4":
+        assert plan.info["t_tile"] == 128, plan.info          # the 4-pixel-per-lane DAS variant ran
     x = torch.from_numpy(np.ascontiguousarray(sig)).cuda()
     das = plan.beamform(x, dm.RAW(dm.KIND_DAS) | dm.ENV(dm.KIND_DAS))
     env_only = plan.beamform(x, dm.ENV(dm.KIND_DAS))[("env", "das")].cpu().numpy()

@@ -334,6 +334,50 @@ def test_envelope_properties(golden):
     assert full.shape == (2, 301)
 
 
+def test_envelope_impulse_response_clamp():
+    """Clamp >= 0 (reading Q11, "clamped to be non-negative"), pinned by a closed
+    form: a unit impulse at t0 through the centred FIR gives h[k] at t = t0 + k - c (convolution of
+    a delta with h is h, numpy.convolve), so the envelope is max(h[k], 0) there and 0 elsewhere.
+    The 127-tap Blackman low-pass has 34 negative taps: a rectifier |.| instead of the clamp would
+    return |h[k]| at those samples, a missing clamp h[k] < 0."""
+    h = O.lpf_taps(127, 5000.0, 450e3)
+    neg = np.flatnonzero(h < 0)
+    assert len(neg) == 34
+    T, t0, c = 400, 150, 63
+    y = np.zeros((1, T))
+    y[0, t0] = 1.0
+    e = O.envelope(y, h)[0]
+    expect = np.zeros(T)
+    expect[t0 - c:t0 - c + 127] = np.maximum(np.convolve([1.0], h), 0.0)
+    np.testing.assert_array_equal(e, expect)
+    assert np.all(e[t0 - c + neg] == 0.0)
+    # a negative impulse gives the same envelope (|.| comes before the low-pass, PAPER.md:75)
+    np.testing.assert_array_equal(O.envelope(-y, h)[0], e)
+
+
+def test_envelope_bandpass_orientation():
+    """The band-pass is a centred convolution (out[t] = sum_k h[k] y[t + c - k]),
+    pinned with an asymmetric 3-tap filter [0, 0, 1] (c = 1): out[t] = y[t - 1], a one-sample
+    delay -- numpy.convolve(mode="same") agrees; a correlation would advance by one sample instead.
+    The identity low-pass [1] leaves |y| visible."""
+    rng = np.random.default_rng(13)
+    y = rng.standard_normal((2, 50))
+    bp = np.array([0.0, 0.0, 1.0])
+    out = O.envelope(y, np.array([1.0]), bp_taps=bp)
+    expect = np.zeros_like(y)
+    expect[:, 1:] = np.abs(y[:, :-1])
+    np.testing.assert_array_equal(out, expect)
+    for r in range(2):
+        np.testing.assert_array_equal(out[r], np.abs(np.convolve(y[r], bp, mode="same")))
+    # and a random asymmetric band-pass before the 127-tap low-pass matches numpy.convolve twice
+    bp2 = rng.standard_normal(31)
+    h = O.lpf_taps(127, 5000.0, 450e3)
+    y = rng.standard_normal((2, 300))
+    ref = np.stack([np.maximum(np.convolve(np.abs(np.convolve(y[r], bp2, mode="same")), h, mode="same"), 0)
+                    for r in range(2)])
+    np.testing.assert_allclose(O.envelope(y, h, bp_taps=bp2), ref, rtol=1e-12, atol=1e-14)
+
+
 # ----------------------------------------------------------------- pipeline trend (PAPER.md:201)
 def test_pipeline_peak_and_dynamic_range_trend():
     """Noise-free 32-mic PSF scan (az -90..90 step 2, reflector at az 10 deg, sample
