@@ -9,13 +9,20 @@ p = 2 followed by the 127-tap 5 kHz envelope.  One step = one dmas_beamform call
 256-frame batch (every §8(a) row: signed roots -> gather / power sums / Newton-Girard / CF ->
 envelope); the delay table (A1) is built once per plan, as the paper pre-computes it.
 
-  python bench.py [--gpus N --steps K --warmup W]          # our CUDA path (one process per GPU)
+  python bench.py [--gpus N --steps K --warmup W]          # our CUDA path, one process per GPU
   python bench.py --impl reference ...                      # the float64 oracle on the host cores
+  python bench.py --gpus 2 --dry-run                        # CPU: rank spawning / sharding only
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): frames are independent problems, so every rank
-beamforms its own 256-frame stream over the full grid (weak scaling, no data-path collective);
-the step time is the max over ranks.  ``--mode dirshard`` instead broadcasts one stream from
-rank 0 and splits the direction grid (strong scaling; shards stay resident).
+Multi-GPU (north_star, default `--mode dirshard`): the direction grid is split
+into contiguous slices, one per rank; each step the root's 256-frame recording is broadcast and
+every rank beamforms its slice -- both inside libdmas (a sharded plan, NCCL), the broadcast of
+frame chunk c + 1 overlapped with the compute of chunk c.  `value` keeps the image shards resident
+(the units all ranks processed / the max over ranks of the step time: strong scaling, the total
+work is fixed); the line's `gathered` object times the same step with every image gathered onto
+the root (grouped send / recv per chunk, overlapped with the next chunk).  `--mode weak` instead
+gives every rank its own 256-frame stream over the whole grid (replicas, no exchange).
+With `--gpus N` and no torchrun environment, the script re-launches itself under
+torch.distributed.run with N ranks.
 """
 
 from __future__ import annotations
@@ -23,6 +30,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,7 +48,16 @@ from workloads import gen  # noqa: E402
 METRIC = "CF-DMAS images/sec (directions x range samples per second) at 1/2/4/8 B200"
 UNIT = "px/s"
 LP_TAPS = 127
-FP32_LANES_PER_SM_CLK = 128     # FFMA/FADD/FMUL lanes per SM per clock (B200, measured 124-128)
+FP32_LANES_PER_SM_CLK = 128     # FFMA/FADD/FMUL lanes per SM per clock (guide; tools/ubench_fp32.cu measures it)
+# SURVEY.md §8(d) FLOP convention (FADD/FMUL = 1, FFMA = 2): algorithmic FLOP per pixel of the
+# beamform = N_m * phi_p + 30, phi_p = 5 / 6 / 9 / 10 for p = 2 / 3 / 4 / 5
+PHI_P = {2: 5, 3: 6, 4: 9, 5: 10}
+# FP32-pipe lane-ops per microphone sample of k_beamform_lds64 as issued and per pixel epilogue
+OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
+OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
+BF_KERNELS = {0: "k_beamform", 1: "k_beamform_lds64", 2: "k_beamform_mg"}   # dmas_plan_info.bf_kernel
+ENV_PRECISION = ("tcgen05 low-pass, 3-pass BF16 split: <= 3 * 2^-16 ~ 4.6e-5 of the envelope value (bound); "
+                 "the FP32 FIR (env_engine = 1) is timed in all_fp32")
 
 
 def parse():
@@ -51,9 +69,11 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="frames per step (0: the workload's, C5 256, C4 16)")
     ap.add_argument("--workload", choices=["C5", "C4"], default="C5",
                     help="C5 = the metric's config (default); C4 = 64-mic p = 3 secondary line")
-    ap.add_argument("--mode", choices=["weak", "dirshard"], default="weak")
+    ap.add_argument("--mode", choices=["dirshard", "weak"], default="dirshard")
     ap.add_argument("--bf-engine", type=int, choices=[0, 1], default=0,
                     help="beamform kernel: 0 auto (LDS.64 kernel where it fits), 1 classic k_beamform (comparison)")
+    ap.add_argument("--env-engine", type=int, choices=[0, 1], default=0,
+                    help="envelope low-pass: 0 tcgen05 (BF16 split), 1 the FP32 FIR")
     ap.add_argument("--interp", action="store_true",
                     help="linear-interpolation pre-steering (fractional delays, roots on the fly; NEXT-2)")
     ap.add_argument("--raw", action="store_true",
@@ -62,7 +82,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-dirs", type=int, default=0, help="directions per core in the CPU sample (0 = auto)")
+    ap.add_argument("--no-extras", action="store_true", help="skip all_fp32 / linearity / C1 latency")
+    ap.add_argument("--cpu-dirs", type=int, default=0, help="directions per core in the all-core CPU sample (0 = all)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU only: spawn ranks, shard the grid, print the line")
     return ap.parse_args()
 
 
@@ -71,6 +93,32 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int) -> int:
+    """--gpus N without a torchrun environment: re-launch this script with N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
@@ -83,19 +131,23 @@ def _oracle_chunk(job):
     return e.shape[0] * e.shape[1]
 
 
-def oracle_rate(cfg, frame_idx=0, dirs_per_core=0, cores=None, pool=None):
-    """Time the float64 oracle (as it stands) on a bounded sample of the C5 step: one frame,
-    `cores` x `dirs_per_core` directions (default: the whole frame), all T samples, CF-DMAS +
-    envelope, one process per core over contiguous direction chunks.  The delay table is built
-    outside the timed region, as in the CUDA path's plan.  Returns (px/s, cores, description)."""
+def oracle_rate(cfg, n_dirs, cores, pool=None, frame_idx=0):
+    """Time the float64 oracle (as it stands) on a bounded sample of the step: one frame, `n_dirs`
+    directions spread over the grid, all T samples, CF-DMAS + envelope, split over `cores`
+    processes (contiguous direction chunks).  The delay table is built outside the timed region,
+    as in the CUDA path's plan.  Returns (px/s, seconds, px)."""
     import multiprocessing as mp
     from oracle import dmas_oracle as O
-    cores = cores or os.cpu_count() or 1
-    dpc = dirs_per_core or max(1, -(-len(cfg["dirs"]) // cores))    # default: one whole frame
-    n = min(len(cfg["dirs"]), cores * dpc)
+    n = min(len(cfg["dirs"]), n_dirs)
     sel = np.linspace(0, len(cfg["dirs"]) - 1, n).astype(int)
     d = O.delay_table(cfg["mic_xyz"], cfg["dirs"][sel], cfg["fs"], cfg["c"])
+    dpc = -(-n // cores)
     jobs = [(cfg["signals"][frame_idx], d[i:i + dpc], cfg["order"]) for i in range(0, n, dpc)]
+    if cores == 1:
+        t0 = time.perf_counter()
+        px = sum(_oracle_chunk(j) for j in jobs)
+        dt = time.perf_counter() - t0
+        return px / dt, dt, px
     own = pool is None
     if own:
         pool = mp.get_context("fork").Pool(cores)
@@ -107,50 +159,78 @@ def oracle_rate(cfg, frame_idx=0, dirs_per_core=0, cores=None, pool=None):
         if own:
             pool.close()
             pool.join()
-    desc = (f"frame {frame_idx} of {cfg['name']}, {n} of {len(cfg['dirs'])} directions x {cfg['T']} samples "
-            f"= {px} px, CF-DMAS p={cfg['order']} + {LP_TAPS}-tap envelope, float64 numpy oracle, "
-            f"{cores} processes; {dt:.1f} s")
-    return px / dt, cores, desc
+    return px / dt, dt, px
+
+
+def cpu_baseline(args):
+    """The oracle on this host (SURVEY.md §8(d) "Oracle"): all cores over one whole frame, one
+    process over 1024 directions, and the linearity check of PAPER.md:284 (time proportional to
+    the number of directions) on one process at 128 / 256 / 512 directions."""
+    cfg = gen.config(args.workload, frames=1)
+    cores = os.cpu_count() or 1
+    n_all = len(cfg["dirs"]) if not args.cpu_dirs else cores * args.cpu_dirs
+    r_all, dt_all, px_all = oracle_rate(cfg, n_all, cores)
+    r_one, dt_one, px_one = oracle_rate(cfg, 1024, 1)
+    lin = {"n_dirs": [], "seconds": [], "px_per_s": []}
+    for n in (128, 256, 512):
+        r, dt, _ = oracle_rate(cfg, n, 1)
+        lin["n_dirs"].append(n)
+        lin["seconds"].append(dt)
+        lin["px_per_s"].append(r)
+    lin["time_ratio_512_vs_128"] = lin["seconds"][2] / lin["seconds"][0]
+    return {"value": r_all, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"frame 0 of {cfg['name']}: {n_all} of {len(cfg['dirs'])} directions x {cfg['T']} samples = "
+                       f"{px_all} px, CF-DMAS p={cfg['order']} + {LP_TAPS}-tap envelope, float64 numpy oracle, "
+                       f"{cores} processes; {dt_all:.1f} s"),
+            "cpu_model": cpu_model(),
+            "single_process": {"value": r_one, "unit": UNIT, "cores": 1,
+                               "sample": f"frame 0, 1024 directions spread over the grid = {px_one} px; {dt_one:.1f} s"},
+            "linearity": lin}
 
 
 def run_reference(args, rank, world):
     """The reference arm: the oracle, as it stands, on the host cores (rank 0 only).  Each step
-    beamforms one whole C5 frame (a bounded sample of the 256-frame step) with a process pool
-    over all cores; value = median px/s over the timed steps."""
+    beamforms one whole frame of the workload (a bounded sample of the 256-frame step) with a
+    process pool over all cores; value = median px/s over the timed steps, ms_per_step = the
+    measured time of one such step."""
     import multiprocessing as mp
     if rank != 0:
         return 0
     cfg = gen.config(args.workload, frames=1)
     cores = os.cpu_count() or 1
-    rates, desc = [], ""
+    n_dirs = len(cfg["dirs"]) if not args.cpu_dirs else cores * args.cpu_dirs
+    rates, secs, px = [], [], 0
     with mp.get_context("fork").Pool(cores) as pool:
         for i in range(args.warmup + args.steps):
-            r, c, desc = oracle_rate(cfg, 0, args.cpu_dirs, cores, pool)
+            r, dt, px = oracle_rate(cfg, n_dirs, cores, pool)
             if i >= args.warmup:
                 rates.append(r)
+                secs.append(dt)
     value = statistics.median(rates)
-    px_step = len(cfg["dirs"]) * cfg["T"] * args.frames
+    sample = (f"each step: frame 0 of {cfg['name']}, {n_dirs} directions x {cfg['T']} samples = {px} px "
+              f"(one frame of the {args.frames}-frame step), CF-DMAS p={cfg['order']} + {LP_TAPS}-tap envelope, "
+              f"float64 numpy oracle, {cores} processes")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * px_step / value,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
+        "higher_is_better": True, "scaling": "strong" if args.mode == "dirshard" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded eRTIS-like point-reflector echoes, matched-filtered; workloads/gen.py)",
         "config": config_dict(args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "each step times one whole C5 frame (a bounded sample of the 256-frame step) on the host cores; "
-                "ms_per_step is that rate extrapolated linearly to the 256-frame step (cost is exactly "
-                "proportional to frames x directions x samples)",
+        "note": "ms_per_step is the measured time of one sample step (one frame, all directions); value is px/s "
+                "of that sample, the same metric and unit as the GPU arm",
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def load_traffic():
-    """DRAM bytes per launch of each kernel from the committed `ncu --set full` capture
-    (profiles/<round>/traffic.json, written from dram__bytes_read.sum + dram__bytes_write.sum)."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def load_profile():
+    """Per-kernel ncu figures from the committed `ncu --set full` capture (profiles/traffic.json:
+    dram__bytes_read.sum + dram__bytes_write.sum per launch, FMA-pipe and issue-slot activity)."""
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f)
     except OSError:
         return {}
@@ -164,24 +244,19 @@ WORKLOADS = {
            "n_samples": 8192, "fs_hz": 450000, "order": 3, "frames": 16,
            "l2": "every step streams 8 GiB of output (no L2 reuse across steps)"},
 }
-# FP32-pipe lane-ops per microphone sample of k_beamform (acc_add<P>) and per pixel
-# epilogue (Newton-Girard + CF + CF product)
-OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
-BF_KERNELS = {0: "k_beamform", 1: "k_beamform_lds64", 2: "k_beamform_mg"}   # dmas_plan_info.bf_kernel
-OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
 
 
 def config_dict(args, world):
+    """The workload; identical for both arms."""
     w = WORKLOADS[args.workload]
     return {"workload": args.workload, "array": w["array"], "n_dirs": w["n_dirs"], "grid": w["grid"],
             "n_samples": w["n_samples"], "fs_hz": w["fs_hz"], "order": w["order"],
-            "frames_per_step_per_gpu": args.frames,
+            "frames_per_step": args.frames,
             "outputs": f"CF-DMAS{w['order']} envelope (127-tap 5 kHz low-pass)",
             "mode": args.mode, "world": world, "l2": w["l2"],
             "input": "raw recordings, matched filter on the GPU (1125-tap chirp)" if args.raw
                      else "matched-filtered signals (north_star input)",
-            "presteer": "linear interpolation (fractional delays)" if args.interp else "nearest sample (integer LUT)",
-            "beamform_kernel": "classic k_beamform (forced)" if args.bf_engine == 1 else "auto"}
+            "presteer": "linear interpolation (fractional delays)" if args.interp else "nearest sample (integer LUT)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -231,13 +306,40 @@ def physical_gpu_index(local: int) -> int:
     return local
 
 
+def step_stats(ms_list):
+    s = sorted(ms_list)
+    p90 = s[min(len(s) - 1, int(round(0.9 * (len(s) - 1))))]
+    return {"median": statistics.median(s), "min": s[0], "p90": p90, "max": s[-1], "n": len(s)}
+
+
+# ------------------------------------------------------------------ dry run (CPU: spawning / sharding)
+def run_dry(args, rank, world):
+    import torch.distributed as dist
+    from paper_2511_09165_b200 import parallel
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_dirs = WORKLOADS[args.workload]["n_dirs"]
+    g0, g1 = parallel.partition(n_dirs, world, rank)
+    cid = parallel.share_comm_id(lambda: os.urandom(128)) if world > 1 else os.urandom(128)
+    info = {"rank": rank, "shard": [g0, g1], "comm_id_head": cid[:8].hex(), "pid": os.getpid()}
+    seen = [None] * world
+    if world > 1:
+        dist.all_gather_object(seen, info)
+    else:
+        seen = [info]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+                          "ranks": seen, "config": config_dict(args, world)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_cfg = gen.config(args.workload, frames=1)
-        r, c, desc = oracle_rate(cpu_cfg, 0, args.cpu_dirs, None)
-        cpu = {"value": r, "unit": UNIT, "cores": c, "kind": "oracle", "sample": desc}
+        cpu = cpu_baseline(args)
 
     import torch
     import torch.distributed as dist
@@ -247,166 +349,303 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    sharded = args.mode == "dirshard" and world > 1
 
     # ---- inputs (resident in HBM before the timed region)
+    F = args.frames
     if args.raw:
-        cfg = gen.raw_config(args.workload, frames=args.frames)
-        dirs = cfg["dirs"]
-        x = torch.from_numpy(cfg["signals"]).to(dev)
+        cfg = gen.raw_config(args.workload, frames=F)
     elif args.mode == "weak":
-        cfg = gen.config(args.workload, frames=args.frames, stream=rank)
-        dirs = cfg["dirs"]
-        x = torch.from_numpy(cfg["signals"]).to(dev)
+        cfg = gen.config(args.workload, frames=F, stream=rank)
     else:
-        cfg = (gen.config(args.workload, frames=args.frames, stream=0) if rank == 0
-               else gen.config(args.workload, frames=1))
-        g0, g1 = parallel.partition(len(cfg["dirs"]), world, rank)
-        dirs = cfg["dirs"][g0:g1]
-        x = torch.empty((args.frames, cfg["mic_xyz"].shape[0], cfg["T"]), dtype=torch.float32, device=dev)
-        if rank == 0:
-            x.copy_(torch.from_numpy(cfg["signals"]))
-    F, T, p = args.frames, cfg["T"], cfg["order"]
-    plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, max_frames=F, lp_taps=LP_TAPS, device=local,
-                     mf_coeffs=cfg.get("chirp") if args.raw else None, delay_interp=1 if args.interp else 0, bf_engine=args.bf_engine)
+        cfg = gen.config(args.workload, frames=F if rank == 0 else 1)   # the recording lives on the root
+    dirs, T, p = cfg["dirs"], cfg["T"], cfg["order"]
+    n_mics = cfg["mic_xyz"].shape[0]
+    x = torch.empty((F,) + cfg["signals"].shape[1:], dtype=torch.float32, device=dev)
+    if rank == 0 or not sharded:
+        x.copy_(torch.from_numpy(cfg["signals"]))
+    kw = dict(max_frames=F, lp_taps=LP_TAPS, mf_coeffs=cfg.get("chirp") if args.raw else None,
+              delay_interp=1 if args.interp else 0, bf_engine=args.bf_engine, env_engine=args.env_engine)
+    if sharded:
+        sb = parallel.ShardedBeamformer(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, device=local, **kw)
+        plan = sb.plan
+    else:
+        plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, device=local, **kw)
     bf_name = BF_KERNELS[plan.info["bf_kernel"]]
     what = dmas.ENV(dmas.KIND_CFDMAS)
-    out = torch.empty((F, len(dirs), T), dtype=torch.float32, device=dev)
+    out = torch.empty((F, plan.n_dirs, T), dtype=torch.float32, device=dev)    # this rank's rows
     stream = torch.cuda.current_stream()
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed_steps(fn, n):
+        """n steps bracketed by a barrier + synchronize on both sides; per-step CUDA events on the
+        launching stream; returns (total ms max over ranks, per-step ms of this rank)."""
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        evs[0].record(stream)
+        for i in range(n):
+            fn()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(n)]
+        total = evs[0].elapsed_time(evs[-1])
+        if world > 1:
+            t = torch.tensor([total], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        barrier()
+        return total, per
+
     def step():
-        if args.mode == "dirshard" and world > 1:
-            dist.broadcast(x, src=0)          # signals broadcast once per step over NVLink (NCCL)
-        plan.beamform(x, what, outs=[out])
+        plan.beamform(x, what, outs=[out])     # sharded: broadcast from the root inside, shards resident
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-
     clocks = ClockSampler(physical_gpu_index(local))
     time.sleep(0.3)
     plan.set_timing(True)
     n_launch0 = dmas.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    total_ms, per_ms = timed_steps(step, args.steps)
     launches = dmas.launch_count() - n_launch0
     plan.set_timing(False)
     ktime = plan.timing_read()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        if dist.get_rank() == 0 and clk is not None:
-            pass
-    n_dirs_total = len(cfg["dirs"]) if args.mode == "dirshard" else len(cfg["dirs"]) * world
-    px_step = F * n_dirs_total * T
+    ms = total_ms / args.steps
+    n_dirs_total = len(dirs)
+    px_step = F * n_dirs_total * T * (world if args.mode == "weak" else 1)
     value = px_step / (ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (device time inside the timed region)
+    # ---- roofline of the dominant kernel (device time inside the timed region, this rank)
     bf_ms, bf_n = ktime["beamform"]
     env_ms, env_n = ktime["envelope"]
     rt_ms, rt_n = ktime["signed_roots"]
-    px_launch_bf = (F * len(dirs) * T) / max(1, bf_n / args.steps)   # pixels per beamform launch
-    n_mics = cfg["mic_xyz"].shape[0]
-    ops_bf = OPS_PER_MIC[p] * n_mics + OPS_EPI[p]   # FP32 pipe lane-ops per pixel
-    ops_env = LP_TAPS                            # one FFMA per tap per pixel
-    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
-    peak_top = FP32_LANES_PER_SM_CLK * sm_count * sm_max * 1e6 / 1e12     # T lane-ops/s at max clock
+    px_rank = F * plan.n_dirs * T
+    px_launch_bf = px_rank / max(1, bf_n / args.steps)
+    px_launch_env = px_rank / max(1, env_n / args.steps)
     bf_avg = bf_ms / max(1, bf_n)
     env_avg = env_ms / max(1, env_n)
-    px_launch_env = (F * len(dirs) * T) / max(1, env_n / args.steps)
-    ach_bf = ops_bf * px_launch_bf / (bf_avg * 1e-3) / 1e12
-    ach_env = ops_env * px_launch_env / (env_avg * 1e-3) / 1e12
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
+    lane_peak = FP32_LANES_PER_SM_CLK * sm_count * sm_max * 1e6 / 1e12      # T lane-ops/s at max clock
+    flop_peak = 2.0 * lane_peak                                            # TFLOP/s, FFMA = 2
+    flop_px = n_mics * PHI_P[p] + 30                                        # SURVEY §8(d), beamform only
+    ach_flop = flop_px * px_launch_bf / (bf_avg * 1e-3) / 1e12
+    ops_px = OPS_PER_MIC[p] * n_mics + OPS_EPI[p]
+    ach_ops = ops_px * px_launch_bf / (bf_avg * 1e-3) / 1e12
     hbm_peak = 6547.2
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             hbm_peak = float(json.load(f)["hbm_gbs"])
     except (OSError, KeyError, ValueError):
         pass
-    env_gbs = 8.0 * px_launch_env / (env_avg * 1e-3) / 1e9          # read raw + write envelope, 4 B each
-    traffic = load_traffic()
-    dom = "beamform" if bf_ms >= env_ms else "envelope"
-    tr = traffic.get(f"k_{dom}", {})
+    env_gbs = 8.0 * px_launch_env / (env_avg * 1e-3) / 1e9 if env_n else 0.0   # read raw + write envelope
+    prof = load_profile()
     frames_launch = F / max(1, bf_n / args.steps)
-    traffic_launch = (tr["dram_bytes_per_launch"] * frames_launch / tr["frames_per_launch"]
-                      if tr.get("dram_bytes_per_launch") and tr.get("frames_per_launch") else None)
-    if dom == "beamform":
-        roofline = {"bound": "alu", "kernel": bf_name, "achieved": ach_bf, "peak": peak_top,
-                    "unit": "Top/s (FP32 lane-ops)", "frac": ach_bf / peak_top}
-    else:
-        roofline = {"bound": "hbm", "kernel": "k_envelope_tc", "achieved": env_gbs, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": env_gbs / hbm_peak}
-    roofline.update({"traffic": traffic_launch,
-                     "traffic_unit": "bytes per launch (ncu dram read+write, scaled to this launch's frames)",
-                     "algorithmic_bytes": 4.0 * px_launch_bf if dom == "beamform" else 8.0 * px_launch_env,
-                "peak_basis": (f"{FP32_LANES_PER_SM_CLK} FP32 lanes/clk/SM x {sm_count} SMs x {sm_max:.0f} MHz "
-                               "(guide unit counts; measured 124/128 in round-1 microbenchmark)") if dom == "beamform"
-                              else "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
-                "kernels": {
-                    "beamform": {"avg_ms": bf_avg, "launches": bf_n, "share": bf_ms / (ms * args.steps),
-                                 "ops_per_px": ops_bf, "Top_s": ach_bf, "frac": ach_bf / peak_top,
-                                 "Gpx_s": px_launch_bf / (bf_avg * 1e-3) / 1e9},
-                    "envelope": {"avg_ms": env_avg, "launches": env_n, "share": env_ms / (ms * args.steps),
-                                 "bound": "hbm", "GB_s": env_gbs, "hbm_frac": env_gbs / hbm_peak,
-                                 "algorithmic_bytes_per_px": 8, "Gpx_s": px_launch_env / (env_avg * 1e-3) / 1e9},
-                    "signed_roots": {"avg_ms": rt_ms / max(1, rt_n), "launches": rt_n,
-                                     "share": rt_ms / (ms * args.steps)}}})
+    pb = prof.get("k_beamform", {})
+    traffic_launch = (pb["dram_bytes_per_launch"] * frames_launch / pb["frames_per_launch"]
+                      if pb.get("dram_bytes_per_launch") and pb.get("frames_per_launch") else None)
+    roofline = {
+        "bound": "alu", "kernel": bf_name, "achieved": ach_flop, "peak": flop_peak,
+        "unit": "TFLOP/s (FP32, FFMA = 2)", "frac": ach_flop / flop_peak, "traffic": traffic_launch,
+        "traffic_unit": "bytes per launch (ncu dram read+write, scaled to this launch's frames)",
+        "algorithmic_bytes": 4.0 * px_launch_bf,
+        "flop_per_px": flop_px,
+        "flop_basis": f"SURVEY.md §8(d): N_m * phi_p + 30 = {n_mics} * {PHI_P[p]} + 30 (FADD/FMUL = 1, FFMA = 2)",
+        "peak_basis": (f"{FP32_LANES_PER_SM_CLK} FP32 lanes/clk/SM x 2 x {sm_count} SMs x {sm_max:.0f} MHz "
+                       "(guide unit counts at the max SM clock; tools/ubench_fp32.cu measures lanes/clk, "
+                       "profiles/r02/ubench.json)"),
+        "issue": {"lane_ops_per_px": ops_px, "T_lane_ops_s": ach_ops, "frac_of_lane_peak": ach_ops / lane_peak,
+                  "formulation_flop_ceiling": PHI_P[p] / (2.0 * OPS_PER_MIC[p]),
+                  "ncu_fma_pipe_pct": pb.get("pipe_fma_pct"), "ncu_issue_active_pct": pb.get("issue_active_pct"),
+                  "note": "the kernel issues 5 FP32 instructions per mic-pixel at p = 2 (x = s|s| is recomputed "
+                          "from the one staged root plane), of which the §8(d) count credits 5 FLOP: its FLOP "
+                          "fraction cannot exceed phi_p / (2 * ops) = 0.5"},
+        "kernels": {
+            "beamform": {"avg_ms": bf_avg, "launches": bf_n, "share": bf_ms / total_ms,
+                         "Gpx_s": px_launch_bf / (bf_avg * 1e-3) / 1e9, "TFLOP_s": ach_flop,
+                         "frac": ach_flop / flop_peak},
+            "envelope": {"avg_ms": env_avg, "launches": env_n, "share": env_ms / total_ms, "bound": "hbm",
+                         "GB_s": env_gbs, "hbm_frac": env_gbs / hbm_peak, "algorithmic_bytes_per_px": 8,
+                         "Gpx_s": px_launch_env / (env_avg * 1e-3) / 1e9 if env_n else None,
+                         "engine": "FP32 FIR" if args.env_engine else "tcgen05 BF16x3",
+                         "ncu_dram_bytes_per_launch": prof.get("k_envelope", {}).get("dram_bytes_per_launch"),
+                         "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"},
+            "signed_roots": {"avg_ms": rt_ms / max(1, rt_n), "launches": rt_n, "share": rt_ms / total_ms}}}
+
+    # ---- sharded: the same step with every image gathered onto the root (overlapped per chunk)
+    gathered = None
+    if sharded:
+        out_full = torch.empty((F, n_dirs_total, T), dtype=torch.float32, device=dev) if rank == 0 else None
+
+        def step_g():
+            plan.beamform(x, what | dmas.GATHER, outs=[out_full] if rank == 0 else None)
+
+        step_g()
+        ng = max(1, min(args.steps, 3))
+        tg, per_g = timed_steps(step_g, ng)
+        gathered = {"value": px_step / (tg / ng * 1e-3), "unit": UNIT, "ms_per_step": tg / ng, "steps": ng,
+                    "gather_bytes_to_root_per_step": int(F * (n_dirs_total - plan.n_dirs) * T * 4),
+                    "note": "broadcast + compute + grouped ncclSend/ncclRecv of every chunk's shards into the "
+                            "root's image, overlapped with the next chunk; root link-bound"}
+        del out_full
 
     # ---- end to end through the public API with host buffers (pinned), copies in the timed region
     e2e = None
-    if not args.no_e2e and args.mode == "weak" and not args.raw:
+    if not args.no_e2e and not args.raw:
         Fe = min(args.e2e_frames, F)
-        hsig = torch.from_numpy(cfg["signals"][:Fe]).pin_memory()
-        hout = torch.empty((Fe, len(dirs), T), dtype=torch.float32).pin_memory()
-        sig_np = hsig.numpy()
-        plan.beamform_host(sig_np, what, outs=[hout.numpy()])           # warm-up (allocates staging)
-        if world > 1:
-            dist.barrier()
+        host_io = rank == 0 or not sharded
+        if host_io:
+            hsig = torch.from_numpy(np.ascontiguousarray(cfg["signals"][:Fe])).pin_memory()
+            hout = torch.empty((Fe, n_dirs_total if sharded else plan.n_dirs, T), dtype=torch.float32).pin_memory()
+
+        def call_host():
+            if host_io:
+                plan.beamform_host(hsig.numpy(), what, outs=[hout.numpy()])
+            else:
+                plan.beamform_host(None, what, n_frames=Fe)
+
+        call_host()                                   # warm-up (allocates the staging)
         times = []
         for _ in range(args.e2e_steps):
+            barrier()
             t0 = time.perf_counter()
-            plan.beamform_host(sig_np, what, outs=[hout.numpy()])
+            call_host()
             times.append(time.perf_counter() - t0)
         et = statistics.median(times)
         if world > 1:
             t = torch.tensor([et], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             et = float(t.item())
-        e2e = {"value": Fe * len(dirs) * T * world / et, "unit": UNIT,
-               "h2d_bytes_per_step": int(hsig.numel() * 4), "d2h_bytes_per_step": int(hout.numel() * 4),
-               "frames_per_step": Fe, "timing": "host wall clock around the synchronous dmas_beamform_host call "
-                                                "(pinned host buffers; H2D, kernels and D2H pipelined in chunks)"}
+        e_px = Fe * n_dirs_total * T * (world if args.mode == "weak" else 1)
+        e2e = {"value": e_px / et, "unit": UNIT,
+               "h2d_bytes_per_step": int(Fe * n_mics * T * 4) * (world if args.mode == "weak" else 1),
+               "d2h_bytes_per_step": int(e_px * 4), "frames_per_step": Fe,
+               "ratio_to_device_value": (e_px / et) / value,
+               "timing": "host wall clock around the synchronous dmas_beamform_host call (pinned host buffers; "
+                         "H2D, kernels and D2H pipelined in chunks; sharded: the root's buffers, images gathered "
+                         "onto the root); bound by the PCIe device-to-host copy of fp32 images"}
+
+    # ---- extras on one GPU: all-FP32 step, linearity in N_psi (PAPER.md:284), C1 launch latency
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras and not args.raw:
+        extras = gpu_extras(args, cfg, plan, x, out, kw, dmas, torch, dev, stream, value)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak" if args.mode == "weak" else "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if args.mode == "dirshard" else "weak", "vs_baseline": None,
+            "dtype": "f32" + ("" if args.env_engine else "+bf16x3(tcgen05 envelope)"),
+            "dtype_detail": ("beamform A2-A4 in FP32 (delay table A1 in FP64); " +
+                             ("envelope FP32 FIR" if args.env_engine else ENV_PRECISION)),
             "data": "synthetic (seeded eRTIS-like point-reflector echoes, matched-filtered; workloads/gen.py)",
-            "config": dict(config_dict(args, world), beamform_kernel=bf_name), "frames_per_s": F * (world if args.mode == "weak" else 1) / (ms * 1e-3),
+            "config": config_dict(args, world), "beamform_kernel": bf_name,
+            "frames_per_s": F * (world if args.mode == "weak" else 1) / (ms * 1e-3),
+            "step_ms": step_stats(per_ms),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
+        if gathered:
+            line["gathered"] = gathered
+        line.update(extras)
         print(json.dumps(line), flush=True)
-    plan.close()
+    if sharded:
+        sb.close()
+    else:
+        plan.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def gpu_extras(args, cfg, plan, x, out, kw, dmas, torch, dev, stream, value):
+    """(1) the same step with the FP32 FIR envelope (env_engine = 1: every multiply FP32);
+    (2) time against N_psi on the GPU ("linear"): the first 4096 / 8192 / 16384
+    directions, 64 frames; (3) C1 (BASELINE configs[0], 93 k pixels per frame: launch-latency
+    bound) per-frame latency, eager calls vs one CUDA-graph replay of 100 single-frame calls."""
+    F, T, p = x.shape[0], cfg["T"], cfg["order"]
+    what = dmas.ENV(dmas.KIND_CFDMAS)
+    res = {}
+
+    def time_fn(fn, n, warm=1):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    if args.env_engine == 0:
+        p32 = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], p, T, device=dev.index,
+                        **dict(kw, env_engine=1))
+        ms32 = time_fn(lambda: p32.beamform(x, what, outs=[out]), 3)
+        res["all_fp32"] = {"value": F * len(cfg["dirs"]) * T / (ms32 * 1e-3), "unit": UNIT, "ms_per_step": ms32,
+                           "steps": 3, "env_engine": 1,
+                           "note": "same step, envelope low-pass as the FP32 FIR (k_envelope_lp127): no BF16 anywhere"}
+        p32.close()
+
+    lin = {"n_dirs": [], "ms": [], "px_per_s": [], "frames": 64}
+    flat = out.view(-1)
+    for n in (4096, 8192, 16384):
+        pl = dmas.Plan(cfg["mic_xyz"], cfg["dirs"][:n], cfg["fs"], cfg["c"], p, T, device=dev.index,
+                       **dict(kw, max_frames=64))
+        o = flat[:64 * n * T].view(64, n, T)
+        xs = x[:64]
+        t = time_fn(lambda: pl.beamform(xs, what, outs=[o]), 3)
+        lin["n_dirs"].append(n)
+        lin["ms"].append(t)
+        lin["px_per_s"].append(64 * n * T / (t * 1e-3))
+        pl.close()
+    lin["time_ratio_16384_vs_4096"] = lin["ms"][2] / lin["ms"][0]
+    res["linearity_gpu"] = lin
+
+    c1 = gen.config("C1")
+    pc = dmas.Plan(c1["mic_xyz"], c1["dirs"], c1["fs"], c1["c"], c1["order"], c1["T"], device=dev.index,
+                   max_frames=1)
+    xc = torch.from_numpy(c1["signals"]).to(dev)
+    oc = torch.empty((1, len(c1["dirs"]), c1["T"]), dtype=torch.float32, device=dev)
+    n_rep = 100
+    eager = time_fn(lambda: pc.beamform(xc, what, outs=[oc]), n_rep, warm=3)
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        pc.beamform(xc, what, outs=[oc])          # warm-up on the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(n_rep):
+                pc.beamform(xc, what, outs=[oc])
+    torch.cuda.synchronize()
+    graph = time_fn(g.replay, 5) / n_rep
+    res["latency_C1"] = {"eager_us_per_frame": 1e3 * eager, "graph_us_per_frame": 1e3 * graph,
+                         "frames": n_rep, "px_per_frame": len(c1["dirs"]) * c1["T"],
+                         "kernels_per_frame": 3,
+                         "note": "C1: 8-mic ULA, 91 directions, T = 1024, CF-DMAS2 envelope; one dmas_beamform call "
+                                 "per frame (roots, beamform, envelope); graph = 100 calls captured once, replayed"}
+    pc.close()
+    return res
 
 
 def main():
     args = parse()
     if args.frames <= 0:
         args.frames = WORKLOADS[args.workload]["frames"]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

@@ -52,7 +52,8 @@ typedef enum {
   DMAS_ERR_SHAPE = 4,   /* n_frames<0 or > max_frames; output mask asks for nothing / for an
                            envelope on a plan built with lp_taps == 0; misaligned pointer         */
   DMAS_ERR_CUDA = 5,    /* CUDA runtime/launch error (message in dmas_last_error())               */
-  DMAS_ERR_OOM = 6      /* device or pinned host allocation failed                                 */
+  DMAS_ERR_OOM = 6,     /* device or pinned host allocation failed                                 */
+  DMAS_ERR_NCCL = 7     /* sharded plans: NCCL missing, communicator setup or a collective failed  */
 } dmas_status;
 
 /* Output image kinds (bit order = order of the `outs` arrays below). */
@@ -64,9 +65,17 @@ enum {
   DMAS_KIND_CF = 16,    /* CF = (sum x)^2 / (N sum x^2 + eps)  */
   DMAS_KIND_ALL = 31
 };
-/* `what` = raw-stage kinds | (envelope-stage kinds << 8). */
+/* `what` = raw-stage kinds | (envelope-stage kinds << 8) | flags. */
 #define DMAS_RAW(kinds) ((uint32_t)(kinds))
 #define DMAS_ENV(kinds) (((uint32_t)(kinds)) << 8)
+/* Flags for direction-sharded plans (n_ranks > 1 or a comm_id; ignored by single-GPU plans):
+   DMAS_GATHER: gather every requested image onto the root rank (full [F][n_dirs][.] buffers there,
+   `outs` ignored on the other ranks); without it each rank's `outs` are its own shard
+   [F][n_local][.] (shards stay resident).  DMAS_SIGNALS_RESIDENT: every rank already holds the
+   signals, skip the broadcast from the root. */
+#define DMAS_GATHER (1u << 16)
+#define DMAS_SIGNALS_RESIDENT (1u << 17)
+#define DMAS_COMM_ID_BYTES 128
 
 typedef struct {
   /* Geometry (host memory, caller-owned, copied by dmas_plan). */
@@ -116,6 +125,18 @@ typedef struct {
                                 one 8-byte shared load per 2 pixels -- when delays are integer and
                                 its windows fit two CTAs per SM, else the classic one); 1 = always
                                 the classic kernel.  Both give bit-identical images.           */
+  /* Direction sharding over GPUs, one process per GPU (north_star: "the
+     direction grid is partitioned across the GPUs ...; signals are broadcast once and image tiles
+     gathered with NCCL").  Every rank passes the SAME descriptor (whole array, whole grid) with
+     its own `rank` and `device`; the plan keeps the contiguous slice dmas_shard_range() gives it
+     and joins an NCCL communicator (created collectively inside dmas_plan: all ranks must call it).
+     n_ranks == 0 and comm_id == NULL: a single-GPU plan (default).  A comm_id with n_ranks == 1 is
+     a one-rank sharded plan (same images; exercises the exchange code on one GPU). */
+  int32_t n_ranks;           /* ranks (processes / GPUs) sharing the grid; 0 or 1 = one          */
+  int32_t rank;              /* this process's rank in [0, n_ranks)                              */
+  int32_t root;              /* rank holding the signals and receiving gathered images           */
+  const uint8_t* comm_id;    /* DMAS_COMM_ID_BYTES from dmas_comm_id() on one rank, shared with
+                                every rank out of band (e.g. a torch.distributed broadcast)      */
 } dmas_plan_desc;
 
 /* Fill `desc` with defaults (zero geometry; order 2; cf_eps 1e-30; lp 127 taps at 5 kHz;
@@ -131,6 +152,13 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out);
 
 /* Beamform n_frames frames, asynchronously on `cuda_stream` (a cudaStream_t; NULL = legacy
    default stream).  Returns after enqueueing.
+   Sharded plans: a collective -- every rank makes the same sequence of calls with the same
+   n_frames and `what`.  `signals` is a device buffer of the full shape on every rank: the root's
+   holds the recording, the others' is overwritten by the root's (ncclBroadcast per frame chunk,
+   overlapped with the previous chunk's compute) unless DMAS_SIGNALS_RESIDENT.  `outs` are the
+   rank's shards [n_frames][n_local][.], or with DMAS_GATHER full images on the root (assembled
+   by grouped ncclSend / ncclRecv of each chunk, overlapped with the next chunk's compute; NULL
+   allowed on the other ranks).  Shards are bitwise the rows a single-GPU plan computes.
      signals : DEVICE, fp32 [n_frames][n_mics][n_samples] (or [.][.][n_samples + mf_taps - 1] raw
                samples when the plan has a matched filter), t contiguous, caller-owned, read-only.
      outs    : HOST array of DEVICE pointers, one per requested (stage, kind): first the raw kinds
@@ -151,7 +179,7 @@ dmas_status dmas_beamform_host(dmas_plan_t plan, const float* host_signals, int3
                                float* const* host_outs, uint32_t what);
 
 /* Copy the plan's integer delay table into host memory int32 [n_dirs][n_mics] (nearest sample,
-   or floor(v) when delay_interp == 1). */
+   or floor(v) when delay_interp == 1); sharded plans: the rank's own rows [n_local][n_mics]. */
 dmas_status dmas_delay_table(dmas_plan_t plan, int32_t* host_out);
 
 /* delay_interp == 1 plans only: the fractional parts a = v - floor(v) in [0, 1), fp32
@@ -159,7 +187,8 @@ dmas_status dmas_delay_table(dmas_plan_t plan, int32_t* host_out);
 dmas_status dmas_delay_fraction(dmas_plan_t plan, float* host_out);
 
 typedef struct {
-  int64_t n_dirs, n_samples, n_out_samples; /* n_out_samples = ceil(T / env_decim)            */
+  int64_t n_dirs, n_samples, n_out_samples; /* n_out_samples = ceil(T / env_decim); n_dirs = the
+                                               plan's own rows (the rank's shard when sharded) */
   int32_t n_mics, order, lp_taps, env_decim, device;
   int32_t d_min, d_max;       /* range of the delay table (samples)                          */
   int32_t psi_tile, t_tile;   /* beamform CTA tile: directions x samples                     */
@@ -172,6 +201,10 @@ typedef struct {
   int32_t tile_order;         /* 0: CTA tiles are runs of consecutive directions; 1: compact
                                  patches from recursive bisection of the unit vectors (LDS.64
                                  path; images unaffected)                                        */
+  int64_t n_dirs_total;       /* the whole grid (== n_dirs unless sharded)                       */
+  int64_t dir_begin;          /* first grid row of this plan's shard (0 unless sharded)          */
+  int32_t n_ranks, rank, root;/* 1, 0, 0 unless sharded                                          */
+  int32_t sharded;            /* 1: the plan holds an NCCL communicator                          */
 } dmas_plan_info;
 dmas_status dmas_get_plan_info(dmas_plan_t plan, dmas_plan_info* info);
 
@@ -181,6 +214,37 @@ dmas_status dmas_get_plan_info(dmas_plan_t plan, dmas_plan_info* info);
    1 prologue (signed roots), 2 beamform, 3 envelope) and clears the record. */
 dmas_status dmas_set_timing(dmas_plan_t plan, int32_t enable);
 dmas_status dmas_timing_read(dmas_plan_t plan, double ms_out[4], int64_t count_out[4]);
+
+/* ---- Multi-GPU helpers (host only; no device work) */
+
+/* A fresh NCCL unique id for dmas_plan_desc.comm_id (call on ONE rank, share the bytes).
+   DMAS_ERR_NCCL when libnccl.so.2 cannot be loaded. */
+dmas_status dmas_comm_id(uint8_t id_out[DMAS_COMM_ID_BYTES]);
+
+/* The contiguous slice [*g0, *g1) of n_dirs grid rows that `rank` of `n_ranks` owns: sizes differ
+   by at most one, the first n_dirs % n_ranks ranks hold one more. */
+dmas_status dmas_shard_range(int64_t n_dirs, int32_t n_ranks, int32_t rank, int64_t* g0, int64_t* g1);
+
+/* One point-to-point transfer of a gather (see dmas_gather_schedule). */
+enum { DMAS_XFER_SEND = 0, DMAS_XFER_RECV = 1, DMAS_XFER_COPY = 2 };
+typedef struct {
+  int32_t kind;      /* DMAS_XFER_*                                                              */
+  int32_t peer;      /* the other rank (the root for SEND; the sender for RECV; self for COPY)   */
+  int32_t frame;     /* frame within the chunk                                                   */
+  int32_t reserved;
+  int64_t src_elem;  /* SEND / COPY: float offset into the rank's shard [n_frames][n_local][row]  */
+  int64_t dst_elem;  /* RECV / COPY: float offset into the root's image [n_frames][n_dirs][row]   */
+  int64_t count;     /* floats                                                                    */
+} dmas_xfer;
+
+/* The exact list of transfers `rank` performs when a sharded plan gathers one image of an
+   n_frames chunk (row = floats per image row) onto `root`, in issue order: per frame, per rank,
+   the root RECVs (or COPYs its own) rows [g0_r, g1_r) and each other rank SENDs its rows.  The
+   library executes this list (COPYs as device copies, the rest in one ncclGroupStart/End);
+   exposed so the exchange can be checked without GPUs.  Writes at most `cap` entries to `out`
+   (may be NULL when cap == 0) and the full count to *n_out. */
+dmas_status dmas_gather_schedule(int64_t n_dirs, int32_t n_ranks, int32_t rank, int32_t root, int32_t n_frames,
+                                 int64_t row, dmas_xfer* out, int64_t cap, int64_t* n_out);
 
 /* Total number of kernels this library has launched in the process (all plans). */
 int64_t dmas_launch_count(void);

@@ -12,8 +12,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdmas.so")
 SOURCES = [os.path.join(CSRC, "dmas_kernels.cu"), os.path.join(CSRC, "dmas_envelope_tc.cu"),
-           os.path.join(CSRC, "dmas_plan.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "dmas_kernels.cuh"), os.path.join(ROOT, "include", "dmas.h")]
+           os.path.join(CSRC, "dmas_plan.cpp"), os.path.join(CSRC, "dmas_comm.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, "dmas_kernels.cuh"), os.path.join(CSRC, "dmas_comm.h"),
+                  os.path.join(ROOT, "include", "dmas.h")]
 
 
 def nvcc_path() -> str:
@@ -60,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise subprocess.CalledProcessError(pr.returncode, "nvcc " + obj)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    link = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    link = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)

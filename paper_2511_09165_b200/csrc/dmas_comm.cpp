@@ -1,0 +1,244 @@
+// Multi-GPU exchange of direction-sharded plans: NCCL resolved at run time, the gather schedule.
+// See dmas_comm.h.  NCCL's types come from its header; no link-time dependency.
+
+#include "dmas_comm.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include <nccl.h>
+
+namespace dmas {
+namespace comm {
+
+void shard_range(int64_t n, int32_t n_ranks, int32_t rank, int64_t* g0, int64_t* g1) {
+  const int64_t base = n / n_ranks, extra = n % n_ranks;
+  *g0 = rank * base + std::min<int64_t>(rank, extra);
+  *g1 = *g0 + base + (rank < extra ? 1 : 0);
+}
+
+std::vector<dmas_xfer> gather_schedule(int64_t n_dirs, int32_t n_ranks, int32_t rank, int32_t root, int32_t n_frames,
+                                       int64_t row_elems) {
+  std::vector<dmas_xfer> xs;
+  int64_t my0, my1;
+  shard_range(n_dirs, n_ranks, rank, &my0, &my1);
+  const int64_t my_n = my1 - my0;
+  for (int32_t f = 0; f < n_frames; ++f) {
+    for (int32_t r = 0; r < n_ranks; ++r) {
+      int64_t g0, g1;
+      shard_range(n_dirs, n_ranks, r, &g0, &g1);
+      if (g1 == g0) continue;                                   // more ranks than directions
+      dmas_xfer x{};
+      x.frame = f;
+      x.count = (g1 - g0) * row_elems;
+      if (rank == root && r == root) {
+        x.kind = DMAS_XFER_COPY;
+        x.peer = root;
+        x.src_elem = (int64_t)f * my_n * row_elems;
+        x.dst_elem = ((int64_t)f * n_dirs + g0) * row_elems;
+      } else if (rank == root) {
+        x.kind = DMAS_XFER_RECV;
+        x.peer = r;
+        x.src_elem = -1;
+        x.dst_elem = ((int64_t)f * n_dirs + g0) * row_elems;
+      } else if (r == rank) {
+        x.kind = DMAS_XFER_SEND;
+        x.peer = root;
+        x.src_elem = (int64_t)f * my_n * row_elems;
+        x.dst_elem = -1;
+      } else {
+        continue;
+      }
+      xs.push_back(x);
+    }
+  }
+  return xs;
+}
+
+// ---------------------------------------------------------------------------------- NCCL (dlopen)
+namespace {
+
+struct Api {
+  bool loaded = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+const Api& api() {
+  static Api a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // the NCCL the process already has (torch's) first, so one process never holds two NCCLs
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return;
+    }
+    bool ok = true;
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p) ok = false;
+      return p;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(sym("ncclCommAbort"));
+    a.CommGetAsyncError = reinterpret_cast<decltype(a.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    if (!ok) {
+      a.why = "libnccl.so.2 lacks a required symbol";
+      return;
+    }
+    a.loaded = true;
+  });
+  return a;
+}
+
+dmas_status nccl_fail(ncclResult_t r, const char* what, std::string& err) {
+  const Api& a = api();
+  err = std::string(what) + ": " + (a.GetErrorString ? a.GetErrorString(r) : "NCCL error");
+  return DMAS_ERR_NCCL;
+}
+
+#define NCCL_TRY(expr, what)                                   \
+  do {                                                         \
+    ncclResult_t r_ = (expr);                                  \
+    if (r_ != ncclSuccess) return nccl_fail(r_, what, err);    \
+  } while (0)
+
+}  // namespace
+
+struct Comm {
+  ncclComm_t comm = nullptr;
+  int32_t n_ranks = 1, rank = 0;
+};
+
+dmas_status unique_id(uint8_t out[DMAS_COMM_ID_BYTES], std::string& err) {
+  static_assert(DMAS_COMM_ID_BYTES == NCCL_UNIQUE_ID_BYTES, "comm id size");
+  const Api& a = api();
+  if (!a.loaded) {
+    err = a.why;
+    return DMAS_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  NCCL_TRY(a.GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, id.internal, DMAS_COMM_ID_BYTES);
+  return DMAS_OK;
+}
+
+dmas_status create(const uint8_t id[DMAS_COMM_ID_BYTES], int32_t n_ranks, int32_t rank, Comm** out,
+                   std::string& err) {
+  const Api& a = api();
+  if (!a.loaded) {
+    err = a.why;
+    return DMAS_ERR_NCCL;
+  }
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, DMAS_COMM_ID_BYTES);
+  auto* c = new Comm();
+  c->n_ranks = n_ranks;
+  c->rank = rank;
+  const ncclResult_t r = a.CommInitRank(&c->comm, n_ranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank", err);
+  }
+  *out = c;
+  return DMAS_OK;
+}
+
+void destroy(Comm* c) {
+  if (!c) return;
+  const Api& a = api();
+  if (c->comm && a.loaded) {
+    ncclResult_t ae = ncclSuccess;
+    a.CommGetAsyncError(c->comm, &ae);
+    if (ae != ncclSuccess) a.CommAbort(c->comm);
+    else a.CommDestroy(c->comm);
+  }
+  delete c;
+}
+
+dmas_status broadcast(Comm* c, float* buf, size_t count, int32_t root, cudaStream_t st, std::string& err) {
+  NCCL_TRY(api().Broadcast(buf, buf, count, ncclFloat32, root, c->comm, st), "ncclBroadcast");
+  return DMAS_OK;
+}
+
+dmas_status allreduce_min(Comm* c, int64_t* v, cudaStream_t st, std::string& err) {
+  int64_t* d = nullptr;
+  if (cudaMalloc(&d, sizeof(int64_t)) != cudaSuccess) {
+    err = "cudaMalloc (allreduce scratch)";
+    return DMAS_ERR_OOM;
+  }
+  dmas_status rc = DMAS_OK;
+  if (cudaMemcpyAsync(d, v, sizeof(int64_t), cudaMemcpyHostToDevice, st) != cudaSuccess) rc = DMAS_ERR_CUDA;
+  if (rc == DMAS_OK) {
+    const ncclResult_t r = api().AllReduce(d, d, 1, ncclInt64, ncclMin, c->comm, st);
+    if (r != ncclSuccess) rc = nccl_fail(r, "ncclAllReduce", err);
+  }
+  if (rc == DMAS_OK && (cudaMemcpyAsync(v, d, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                        cudaStreamSynchronize(st) != cudaSuccess)) {
+    err = "allreduce copy-back";
+    rc = DMAS_ERR_CUDA;
+  }
+  cudaFree(d);
+  return rc;
+}
+
+dmas_status run_gather(Comm* c, const std::vector<dmas_xfer>& xs, const float* shard, float* dst, cudaStream_t st,
+                       std::string& err) {
+  const Api& a = api();
+  // local rows first (plain device copies), then every send / recv of the chunk in one NCCL group
+  for (const dmas_xfer& x : xs)
+    if (x.kind == DMAS_XFER_COPY) {
+      const cudaError_t e = cudaMemcpyAsync(dst + x.dst_elem, shard + x.src_elem, (size_t)x.count * sizeof(float),
+                                            cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        err = std::string("gather copy: ") + cudaGetErrorString(e);
+        return DMAS_ERR_CUDA;
+      }
+    }
+  bool any = false;
+  for (const dmas_xfer& x : xs) any |= x.kind != DMAS_XFER_COPY;
+  if (!any) return DMAS_OK;
+  NCCL_TRY(a.GroupStart(), "ncclGroupStart");
+  for (const dmas_xfer& x : xs) {
+    ncclResult_t r = ncclSuccess;
+    if (x.kind == DMAS_XFER_SEND) r = a.Send(shard + x.src_elem, (size_t)x.count, ncclFloat32, x.peer, c->comm, st);
+    else if (x.kind == DMAS_XFER_RECV) r = a.Recv(dst + x.dst_elem, (size_t)x.count, ncclFloat32, x.peer, c->comm, st);
+    if (r != ncclSuccess) {
+      a.GroupEnd();
+      return nccl_fail(r, x.kind == DMAS_XFER_SEND ? "ncclSend" : "ncclRecv", err);
+    }
+  }
+  NCCL_TRY(a.GroupEnd(), "ncclGroupEnd");
+  return DMAS_OK;
+}
+
+}  // namespace comm
+}  // namespace dmas

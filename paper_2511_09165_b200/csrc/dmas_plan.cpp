@@ -16,7 +16,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
+#include "dmas_comm.h"
 #include "dmas_kernels.cuh"
 
 namespace {
@@ -43,6 +45,13 @@ enum { K_DELAY = 0, K_ROOTS = 1, K_BEAMFORM = 2, K_ENVELOPE = 3 };
 struct TimingRec {
   int kernel;
   cudaEvent_t ev0, ev1;
+};
+
+// NVTX range around a host-side enqueue step (SURVEY.md §5 tracing): visible in Nsight Systems /
+// ncu --nvtx; a no-op without a tool attached.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
 };
 
 // Restores the caller's current device on scope exit.
@@ -123,6 +132,18 @@ struct dmas_plan_s {
   cudaEvent_t ev_last = nullptr;
   bool ev_last_recorded = false;
 
+  // direction sharding over ranks; single-GPU plans: comm == nullptr
+  dmas::comm::Comm* comm = nullptr;
+  int32_t n_ranks = 1, rank = 0, root = 0;
+  int64_t n_dirs_total = 0, dir0 = 0, n_local_max = 0;
+  int32_t x_chunk_cap = 1;            // frames per exchange chunk: the minimum over ranks
+  size_t x_scratch_cap = 0;           // envelope scratch: the minimum over ranks
+  cudaStream_t cs = nullptr;          // comm stream: broadcasts and gathers, in one fixed order
+  cudaEvent_t ev_b[2] = {}, ev_c[2] = {}, ev_g[2] = {}, ev_x0 = nullptr, ev_x1 = nullptr;
+  float* d_gst[2] = {nullptr, nullptr};   // gather staging (the rank's shard of one chunk)
+  size_t gst_cap = 0;
+  bool status_exchanged = false;      // plan-time allreduce done (bail must not join it again)
+
   // timing
   bool timing = false;
   std::vector<TimingRec> recs;
@@ -183,6 +204,16 @@ void free_plan_memory(dmas_plan_s* p) {
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
   if (p->ev_last) cudaEventDestroy(p->ev_last);
+  for (int b = 0; b < 2; ++b) {
+    for (cudaEvent_t e : {p->ev_b[b], p->ev_c[b], p->ev_g[b]})
+      if (e) cudaEventDestroy(e);
+    cudaFree(p->d_gst[b]);
+  }
+  for (cudaEvent_t e : {p->ev_x0, p->ev_x1})
+    if (e) cudaEventDestroy(e);
+  if (p->cs) cudaStreamDestroy(p->cs);
+  dmas::comm::destroy(p->comm);
+  p->comm = nullptr;
 
   for (auto& r : p->recs) {
     cudaEventDestroy(r.ev0);
@@ -276,6 +307,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
                           float* const* env_dst, uint32_t env_kinds, cudaStream_t st) {
   // DAS-only requests on the LDS.64 path sum the samples themselves: identity plane (order 1), no
   // roots (the kernel selects its DAS-only variant on the same condition, dmas_kernels.cu)
+  Nvtx range("dmas chunk");
   const bool das_only = raw_dst[0] && !raw_dst[1] && !raw_dst[2] && !raw_dst[3] && !raw_dst[4];
   const int root_order = (p->interp || (das_only && p->paired)) ? 1 : p->order;
   if (p->mf_taps > 0) {
@@ -338,7 +370,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
 dmas_status check_what(dmas_plan_s* p, uint32_t what, uint32_t& raw_k, uint32_t& env_k) {
   raw_k = what & DMAS_KIND_ALL;
   env_k = (what >> 8) & DMAS_KIND_ALL;
-  if (what & ~(uint32_t)(DMAS_RAW(DMAS_KIND_ALL) | DMAS_ENV(DMAS_KIND_ALL)))
+  if (what & ~(uint32_t)(DMAS_RAW(DMAS_KIND_ALL) | DMAS_ENV(DMAS_KIND_ALL) | DMAS_GATHER | DMAS_SIGNALS_RESIDENT))
     return fail(DMAS_ERR_SHAPE, "unknown bits in `what`");
   if (!raw_k && !env_k) return fail(DMAS_ERR_SHAPE, "`what` requests no output");
   if (env_k && p->lp_taps == 0) return fail(DMAS_ERR_SHAPE, "envelope requested on a plan without envelope stage");
@@ -346,16 +378,39 @@ dmas_status check_what(dmas_plan_s* p, uint32_t what, uint32_t& raw_k, uint32_t&
 }
 
 // Core of dmas_beamform on device pointers (caller holds p->mu and the device guard).
+//
+// Frames go through in chunks (the signed-root plane and the envelope scratch hold one chunk).
+// Sharded plans add the exchange on the plan's comm stream `cs`, issued in one
+// fixed order that every rank repeats (NCCL needs the same sequence on all ranks): broadcast of
+// chunks 0 and 1, then per chunk c: [compute c on `st`] -> gather c -> broadcast c + 2.  The
+// broadcast of chunk c + 1 thus overlaps the compute of chunk c, and the gather of chunk c the
+// compute of chunk c + 1 (the shard staging is double-buffered).  The chunk size depends only on
+// quantities every rank shares (allreduced at plan time), so the messages match on all ranks.
 dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_frames, float* const* outs,
-                            uint32_t raw_k, uint32_t env_k, cudaStream_t st) {
-  const float* raw_user[dmas::N_KINDS] = {};
-  float* env_user[dmas::N_KINDS] = {};
+                            uint32_t raw_k, uint32_t env_k, uint32_t flags, cudaStream_t st) {
+  const bool sharded = p->comm != nullptr;
+  const bool gather = sharded && (flags & DMAS_GATHER);
+  const bool bcast = sharded && !(flags & DMAS_SIGNALS_RESIDENT);
+  const bool is_root = p->rank == p->root;
+  // requested outputs in `outs` order: raw kinds, then envelope kinds, in bit order
+  struct Out {
+    int k;
+    bool env;
+    int64_t row;         // floats per image row
+    float* user;         // caller's buffer (nullptr on non-root ranks when gathering)
+    size_t stage_off;    // floats: offset of this output's region in a gather staging buffer
+  };
+  Out o[2 * dmas::N_KINDS];
   int n = 0;
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((raw_k >> k) & 1u) raw_user[k] = outs[n++];
+    if ((raw_k >> k) & 1u) o[n++] = {k, false, p->T, nullptr, 0};
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((env_k >> k) & 1u) env_user[k] = outs[n++];
+    if ((env_k >> k) & 1u) o[n++] = {k, true, p->T_out, nullptr, 0};
+  const bool user_outs = !(gather && !is_root);
+  if (user_outs && !outs) return fail(DMAS_ERR_NULL, "outs is NULL");
   for (int i = 0; i < n; ++i) {
+    if (!user_outs) break;
+    o[i].user = outs[i];
     if (!outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
     if (((uintptr_t)outs[i]) & 3u) return fail(DMAS_ERR_SHAPE, "misaligned output pointer");
   }
@@ -363,30 +418,95 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
   // at least one frame of every kind, so a call never allocates or synchronises)
   const uint32_t env_only = env_k & ~raw_k;
   const int n_scratch = popcount5(env_only);
-  const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
-  int32_t chunk = std::min(p->chunk_cap, n_frames);
+  const int64_t rows_sz = sharded ? p->n_local_max : p->n_dirs;     // identical on every rank
+  const size_t frame_img = (size_t)rows_sz * p->T * sizeof(float);
+  int32_t chunk = std::min(sharded ? p->x_chunk_cap : p->chunk_cap, n_frames);
   if (n_scratch > 0) {
-    const size_t fit = p->scratch_cap / (frame_img * n_scratch);
+    const size_t fit = (sharded ? p->x_scratch_cap : p->scratch_cap) / (frame_img * n_scratch);
     if (fit < 1) return fail(DMAS_ERR_CUDA, "internal: envelope scratch smaller than one frame");
     chunk = (int32_t)std::min<size_t>((size_t)chunk, fit);
   }
-  if (p->ev_last_recorded) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_last, 0));
-  for (int32_t f0 = 0; f0 < n_frames; f0 += chunk) {
-    const int32_t nf = std::min(chunk, n_frames - f0);
+  if (gather) {
+    size_t per_frame = 0;
+    for (int i = 0; i < n; ++i) per_frame += (size_t)rows_sz * o[i].row * sizeof(float);
+    const size_t fit = p->gst_cap / per_frame;
+    if (fit < 1) return fail(DMAS_ERR_SHAPE, "one frame of the requested images exceeds the gather staging");
+    chunk = (int32_t)std::min<size_t>((size_t)chunk, fit);
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      o[i].stage_off = off;
+      off += (size_t)chunk * p->n_dirs * o[i].row;
+    }
+  }
+  const int32_t n_chunks = (n_frames + chunk - 1) / chunk;
+  // under CUDA-graph capture the calls are ordered by the captured stream itself, and an event
+  // recorded outside the capture must not be waited on inside it
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (capturing && sharded) return fail(DMAS_ERR_SHAPE, "sharded plans cannot be captured in a CUDA graph");
+  if (p->ev_last_recorded && !capturing) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_last, 0));
+  std::string err;
+  Nvtx range(sharded ? (gather ? "dmas_beamform sharded+gather" : "dmas_beamform sharded") : "dmas_beamform");
+  auto issue_bcast = [&](int32_t c) -> dmas_status {
+    Nvtx r("dmas broadcast");
+    const int32_t f0 = c * chunk, nf = std::min(chunk, n_frames - f0);
+    float* sig = const_cast<float*>(signals) + (size_t)f0 * p->n_mics * p->T_in;
+    dmas_status rc = dmas::comm::broadcast(p->comm, sig, (size_t)nf * p->n_mics * p->T_in, p->root, p->cs, err);
+    if (rc != DMAS_OK) return fail(rc, err);
+    CUDA_TRY(cudaEventRecord(p->ev_b[c & 1], p->cs));
+    return DMAS_OK;
+  };
+  if (sharded) {
+    CUDA_TRY(cudaEventRecord(p->ev_x0, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->cs, p->ev_x0, 0));
+    for (int32_t c = 0; bcast && c < std::min(2, n_chunks); ++c) {
+      dmas_status rc = issue_bcast(c);
+      if (rc != DMAS_OK) return rc;
+    }
+  }
+  for (int32_t c = 0; c < n_chunks; ++c) {
+    const int32_t f0 = c * chunk, nf = std::min(chunk, n_frames - f0);
+    if (bcast) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_b[c & 1], 0));
+    if (gather && c >= 2) CUDA_TRY(cudaStreamWaitEvent(st, p->ev_g[c & 1], 0));
     float* raw_dst[dmas::N_KINDS] = {};
     float* env_dst[dmas::N_KINDS] = {};
-    int s = 0;
-    for (int k = 0; k < dmas::N_KINDS; ++k) {
-      if ((raw_k >> k) & 1u) raw_dst[k] = const_cast<float*>(raw_user[k]) + (size_t)f0 * p->n_dirs * p->T;
-      else if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
-      if ((env_k >> k) & 1u) env_dst[k] = env_user[k] + (size_t)f0 * p->n_dirs * p->T_out;
+    for (int i = 0; i < n; ++i) {
+      float* dst = gather ? p->d_gst[c & 1] + o[i].stage_off : o[i].user + (size_t)f0 * p->n_dirs * o[i].row;
+      (o[i].env ? env_dst : raw_dst)[o[i].k] = dst;
     }
+    int s = 0;
+    for (int k = 0; k < dmas::N_KINDS; ++k)
+      if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
     const float* sig = signals + (size_t)f0 * p->n_mics * p->T_in;
     dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st);
     if (rc != DMAS_OK) return rc;
+    if (gather) {
+      Nvtx r("dmas gather");
+      CUDA_TRY(cudaEventRecord(p->ev_c[c & 1], st));
+      CUDA_TRY(cudaStreamWaitEvent(p->cs, p->ev_c[c & 1], 0));
+      for (int i = 0; i < n; ++i) {
+        const std::vector<dmas_xfer> xs =
+            dmas::comm::gather_schedule(p->n_dirs_total, p->n_ranks, p->rank, p->root, nf, o[i].row);
+        float* dst = is_root ? o[i].user + (size_t)f0 * p->n_dirs_total * o[i].row : nullptr;
+        rc = dmas::comm::run_gather(p->comm, xs, p->d_gst[c & 1] + o[i].stage_off, dst, p->cs, err);
+        if (rc != DMAS_OK) return fail(rc, err);
+      }
+      CUDA_TRY(cudaEventRecord(p->ev_g[c & 1], p->cs));
+    }
+    if (bcast && c + 2 < n_chunks) {
+      rc = issue_bcast(c + 2);
+      if (rc != DMAS_OK) return rc;
+    }
   }
-  CUDA_TRY(cudaEventRecord(p->ev_last, st));
-  p->ev_last_recorded = true;
+  if (sharded) {
+    CUDA_TRY(cudaEventRecord(p->ev_x1, p->cs));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_x1, 0));
+  }
+  if (!capturing) {
+    CUDA_TRY(cudaEventRecord(p->ev_last, st));
+    p->ev_last_recorded = true;
+  }
   return DMAS_OK;
 }
 
@@ -409,8 +529,26 @@ void dmas_plan_desc_init(dmas_plan_desc* d) {
 dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   if (!out) return fail(DMAS_ERR_NULL, "out is NULL");
   *out = nullptr;
+  Nvtx range("dmas_plan");
   dmas_status st = validate(desc);
   if (st != DMAS_OK) return st;
+  // direction sharding: the plan is built for this rank's contiguous slice of the
+  // grid; everything below sees only the slice
+  const bool sharded = desc->n_ranks > 1 || desc->comm_id != nullptr;
+  const int32_t n_ranks = std::max(1, desc->n_ranks);
+  int64_t g0 = 0, g1 = desc->n_dirs;
+  if (sharded) {
+    if (!desc->comm_id) return fail(DMAS_ERR_NULL, "comm_id is NULL (n_ranks > 1)");
+    if (desc->rank < 0 || desc->rank >= n_ranks) return fail(DMAS_ERR_INVALID, "rank not in [0, n_ranks)");
+    if (desc->root < 0 || desc->root >= n_ranks) return fail(DMAS_ERR_INVALID, "root not in [0, n_ranks)");
+    if (desc->n_dirs < n_ranks) return fail(DMAS_ERR_INVALID, "fewer directions than ranks");
+    dmas::comm::shard_range(desc->n_dirs, n_ranks, desc->rank, &g0, &g1);
+  }
+  dmas_plan_desc local_desc = *desc;
+  local_desc.n_dirs = g1 - g0;
+  local_desc.dir_az_el = desc->dir_az_el + 2 * g0;
+  const dmas_plan_desc* full_desc = desc;
+  desc = &local_desc;
 
   int dev = desc->device;
   if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
@@ -423,6 +561,12 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   p->device = dev;
   p->n_mics = desc->n_mics;
   p->n_dirs = desc->n_dirs;
+  p->n_dirs_total = full_desc->n_dirs;
+  p->dir0 = g0;
+  p->n_ranks = n_ranks;
+  p->rank = sharded ? desc->rank : 0;
+  p->root = sharded ? desc->root : 0;
+  p->n_local_max = (full_desc->n_dirs + n_ranks - 1) / n_ranks;
   p->T = desc->n_samples;
   p->order = desc->order;
   p->max_frames = desc->max_frames;
@@ -438,6 +582,12 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   p->scratch_budget = desc->scratch_bytes > 0 ? desc->scratch_bytes : ((int64_t)4 << 30);
 
   auto bail = [&](dmas_status s) {
+    if (p->comm && !p->status_exchanged) {
+      // the other ranks wait in the plan-time allreduce: contribute "failed" so they fail too
+      int64_t v = 0;
+      std::string ignored;
+      dmas::comm::allreduce_min(p->comm, &v, p->cs, ignored);
+    }
     free_plan_memory(p);
     delete p;
     return s;
@@ -449,6 +599,14 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
       return bail(fail(e_ == cudaErrorMemoryAllocation ? DMAS_ERR_OOM : DMAS_ERR_CUDA,            \
                        std::string(#expr) + ": " + cudaGetErrorString(e_)));                      \
   } while (0)
+  if (sharded) {
+    // the communicator first: every rank reaches this point (validation is identical on all), and
+    // a failure further down is then reported to the others through the plan-time allreduce
+    PLAN_TRY(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
+    std::string err;
+    dmas_status rc = dmas::comm::create(full_desc->comm_id, n_ranks, p->rank, &p->comm, err);
+    if (rc != DMAS_OK) return bail(fail(rc, err));
+  }
 
   // ---- A1: unit vectors on the host (libm, no contraction), table on the device
   const int64_t nd = p->n_dirs;
@@ -790,16 +948,42 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     if (p->lp_tc) PLAN_TRY(dmas::envelope_tc_configure());
     PLAN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev));
     // raw-image scratch for envelope-only kinds: the budget (default 4 GiB), capped at what
-    // max_frames frames of all five kinds need, and never below one frame of every kind
-    const size_t frame_img = (size_t)p->n_dirs * p->T * sizeof(float);
+    // max_frames frames of all five kinds need, and never below one frame of every kind (sharded
+    // plans size it with the largest shard, so the chunking is the same on every rank)
+    const size_t frame_img = (size_t)(sharded ? p->n_local_max : p->n_dirs) * p->T * sizeof(float);
     const size_t all_kinds = frame_img * dmas::N_KINDS;
     size_t cap = std::min<size_t>((size_t)p->scratch_budget, all_kinds * (size_t)p->max_frames);
     cap = std::max(cap, all_kinds);
     PLAN_TRY(cudaMalloc(&p->d_scratch, cap));
     p->scratch_cap = cap;
+    p->x_scratch_cap = cap;
   }
   PLAN_TRY(cudaEventCreateWithFlags(&p->ev_last, cudaEventDisableTiming));
+  if (sharded) {
+    // gather staging: two buffers, each at least one frame of every raw and envelope kind of the
+    // largest shard (and >= 256 MiB so chunks stay long)
+    const size_t frame_max = (size_t)p->n_local_max * (p->T + p->T_out) * sizeof(float) * dmas::N_KINDS;
+    p->gst_cap = std::max(frame_max, (size_t)256 << 20);
+    for (int b = 0; b < 2; ++b) {
+      PLAN_TRY(cudaMalloc(&p->d_gst[b], p->gst_cap));
+      for (cudaEvent_t* e : {&p->ev_b[b], &p->ev_c[b], &p->ev_g[b]})
+        PLAN_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    PLAN_TRY(cudaEventCreateWithFlags(&p->ev_x0, cudaEventDisableTiming));
+    PLAN_TRY(cudaEventCreateWithFlags(&p->ev_x1, cudaEventDisableTiming));
+  }
   PLAN_TRY(cudaDeviceSynchronize());
+  if (sharded) {
+    // every rank built its shard: agree on the frames per exchange chunk (the minimum over ranks);
+    // a rank that failed above contributed 0 from `bail`, so all ranks fail together
+    int64_t v = p->chunk_cap;
+    std::string err;
+    p->status_exchanged = true;
+    dmas_status rc = dmas::comm::allreduce_min(p->comm, &v, p->cs, err);
+    if (rc != DMAS_OK) return bail(fail(rc, err));
+    if (v < 1) return bail(fail(DMAS_ERR_NCCL, "another rank failed to build its plan"));
+    p->x_chunk_cap = (int32_t)v;
+  }
 #undef PLAN_TRY
   *out = p;
   return DMAS_OK;
@@ -814,11 +998,10 @@ dmas_status dmas_beamform(dmas_plan_t p, const float* signals, int32_t n_frames,
   if (st != DMAS_OK) return st;
   if (n_frames == 0) return DMAS_OK;
   if (!signals) return fail(DMAS_ERR_NULL, "signals is NULL");
-  if (!outs) return fail(DMAS_ERR_NULL, "outs is NULL");
   if (((uintptr_t)signals) & 3u) return fail(DMAS_ERR_SHAPE, "misaligned signals pointer");
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard guard(p->device);
-  return beamform_device(p, signals, n_frames, outs, raw_k, env_k, (cudaStream_t)cuda_stream);
+  return beamform_device(p, signals, n_frames, outs, raw_k, env_k, what, (cudaStream_t)cuda_stream);
 }
 
 dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t n_frames, float* const* host_outs,
@@ -829,20 +1012,26 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
   dmas_status st = check_what(p, what, raw_k, env_k);
   if (st != DMAS_OK) return st;
   if (n_frames == 0) return DMAS_OK;
-  if (!host_signals || !host_outs) return fail(DMAS_ERR_NULL, "host buffer is NULL");
+  // sharded plans: the root's host buffers go in and come out; the exchange is the device path's
+  // (broadcast of the root's signals, images gathered onto the root); other ranks pass NULL
+  const bool host_io = p->comm == nullptr || p->rank == p->root;
   const int n_out = popcount5(raw_k) + popcount5(env_k);
-  for (int i = 0; i < n_out; ++i)
-    if (!host_outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
+  if (host_io) {
+    if (!host_signals || !host_outs) return fail(DMAS_ERR_NULL, "host buffer is NULL");
+    for (int i = 0; i < n_out; ++i)
+      if (!host_outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
+  }
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard guard(p->device);
 
   // frames per pipeline stage: bounded by max_frames and ~512 MiB of device output per buffer
+  // (computed from whole-grid sizes, so every rank of a sharded plan takes the same stages)
   std::vector<size_t> out_frame_bytes;
   size_t out_frame_total = 0;
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((raw_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs * p->T * sizeof(float));
+    if ((raw_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs_total * p->T * sizeof(float));
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs * p->T_out * sizeof(float));
+    if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs_total * p->T_out * sizeof(float));
   for (size_t b : out_frame_bytes) out_frame_total += b;
   const size_t sig_frame = (size_t)p->n_mics * p->T_in * sizeof(float);
   int32_t hc = (int32_t)std::max<size_t>(1, ((size_t)512 << 20) / out_frame_total);
@@ -850,7 +1039,8 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
 
   for (auto& s : p->hs)
     if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  if (p->hsig_cap < sig_frame * hc || p->hout_cap < out_frame_total * hc) {
+  // (device staging: kept between calls; non-root ranks of a sharded plan hold no image staging)
+  if (p->hsig_cap < sig_frame * hc || (host_io && p->hout_cap < out_frame_total * hc)) {
     for (int b = 0; b < 2; ++b) {
       cudaFree(p->d_hsig[b]);
       cudaFree(p->d_hout[b]);
@@ -859,10 +1049,10 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
     p->hsig_cap = p->hout_cap = 0;
     for (int b = 0; b < 2; ++b) {
       CUDA_TRY(cudaMalloc(&p->d_hsig[b], sig_frame * hc));
-      CUDA_TRY(cudaMalloc(&p->d_hout[b], out_frame_total * hc));
+      if (host_io) CUDA_TRY(cudaMalloc(&p->d_hout[b], out_frame_total * hc));
     }
     p->hsig_cap = sig_frame * hc;
-    p->hout_cap = out_frame_total * hc;
+    p->hout_cap = host_io ? out_frame_total * hc : 0;
   }
   for (auto& row : p->h_ev)
     for (auto& e : row)
@@ -876,8 +1066,9 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
     const int b = chunk_idx & 1;
     const int32_t nf = std::min(hc, n_frames - f0);
     if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[0], d2h_done[b], 0));
-    CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T_in, sig_frame * nf,
-                             cudaMemcpyHostToDevice, p->hs[0]));
+    if (host_io)
+      CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T_in, sig_frame * nf,
+                               cudaMemcpyHostToDevice, p->hs[0]));
     CUDA_TRY(cudaEventRecord(h2d_done[b], p->hs[0]));
     CUDA_TRY(cudaStreamWaitEvent(p->hs[1], h2d_done[b], 0));
     if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[1], d2h_done[b], 0));
@@ -887,11 +1078,11 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
       douts[i] = p->d_hout[b] + off / sizeof(float);
       off += out_frame_bytes[i] * nf;
     }
-    rc = beamform_device(p, p->d_hsig[b], nf, douts.data(), raw_k, env_k, p->hs[1]);
+    rc = beamform_device(p, p->d_hsig[b], nf, douts.data(), raw_k, env_k, DMAS_GATHER, p->hs[1]);
     if (rc != DMAS_OK) break;
     CUDA_TRY(cudaEventRecord(comp_done[b], p->hs[1]));
     CUDA_TRY(cudaStreamWaitEvent(p->hs[2], comp_done[b], 0));
-    for (size_t i = 0; i < out_frame_bytes.size(); ++i)
+    for (size_t i = 0; host_io && i < out_frame_bytes.size(); ++i)
       CUDA_TRY(cudaMemcpyAsync(host_outs[i] + (size_t)f0 * (out_frame_bytes[i] / sizeof(float)), douts[i],
                                out_frame_bytes[i] * nf, cudaMemcpyDeviceToHost, p->hs[2]));
     CUDA_TRY(cudaEventRecord(d2h_done[b], p->hs[2]));
@@ -935,6 +1126,12 @@ dmas_status dmas_get_plan_info(dmas_plan_t p, dmas_plan_info* info) {
   info->chunk_frames = p->chunk_cap;
   info->bf_kernel = p->paired ? 1 : p->mg > 0 ? 2 : 0;
   info->tile_order = p->d_psi_map ? 1 : 0;
+  info->n_dirs_total = p->n_dirs_total;
+  info->dir_begin = p->dir0;
+  info->n_ranks = p->n_ranks;
+  info->rank = p->rank;
+  info->root = p->root;
+  info->sharded = p->comm ? 1 : 0;
   return DMAS_OK;
 }
 
@@ -970,6 +1167,32 @@ dmas_status dmas_timing_read(dmas_plan_t p, double ms_out[4], int64_t count_out[
 
 int64_t dmas_launch_count(void) { return g_launches.load(); }
 
+dmas_status dmas_comm_id(uint8_t id_out[DMAS_COMM_ID_BYTES]) {
+  if (!id_out) return fail(DMAS_ERR_NULL, "id_out is NULL");
+  std::string err;
+  dmas_status rc = dmas::comm::unique_id(id_out, err);
+  return rc == DMAS_OK ? rc : fail(rc, err);
+}
+
+dmas_status dmas_shard_range(int64_t n_dirs, int32_t n_ranks, int32_t rank, int64_t* g0, int64_t* g1) {
+  if (!g0 || !g1) return fail(DMAS_ERR_NULL, "NULL argument");
+  if (n_dirs < 0 || n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(DMAS_ERR_INVALID, "bad shard arguments");
+  dmas::comm::shard_range(n_dirs, n_ranks, rank, g0, g1);
+  return DMAS_OK;
+}
+
+dmas_status dmas_gather_schedule(int64_t n_dirs, int32_t n_ranks, int32_t rank, int32_t root, int32_t n_frames,
+                                 int64_t row, dmas_xfer* out, int64_t cap, int64_t* n_out) {
+  if (!n_out || (cap > 0 && !out)) return fail(DMAS_ERR_NULL, "NULL argument");
+  if (n_dirs < 1 || n_ranks < 1 || rank < 0 || rank >= n_ranks || root < 0 || root >= n_ranks || n_frames < 0 ||
+      row < 1)
+    return fail(DMAS_ERR_INVALID, "bad gather-schedule arguments");
+  const std::vector<dmas_xfer> xs = dmas::comm::gather_schedule(n_dirs, n_ranks, rank, root, n_frames, row);
+  *n_out = (int64_t)xs.size();
+  for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)xs.size()); ++i) out[i] = xs[(size_t)i];
+  return DMAS_OK;
+}
+
 void dmas_destroy(dmas_plan_t p) {
   if (!p) return;
   {
@@ -990,6 +1213,7 @@ const char* dmas_status_string(dmas_status s) {
     case DMAS_ERR_SHAPE: return "DMAS_ERR_SHAPE";
     case DMAS_ERR_CUDA: return "DMAS_ERR_CUDA";
     case DMAS_ERR_OOM: return "DMAS_ERR_OOM";
+    case DMAS_ERR_NCCL: return "DMAS_ERR_NCCL";
   }
   return "DMAS_ERR_UNKNOWN";
 }

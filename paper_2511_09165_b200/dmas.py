@@ -23,7 +23,11 @@ KIND_BITS = {"das": KIND_DAS, "dmas": KIND_DMAS, "cfdmas": KIND_CFDMAS, "cfdas":
 KIND_ORDER = ("das", "dmas", "cfdmas", "cfdas", "cf")     # bit order = order of `outs`
 
 STATUS = {0: "DMAS_OK", 1: "DMAS_ERR_NULL", 2: "DMAS_ERR_INVALID", 3: "DMAS_ERR_ORDER", 4: "DMAS_ERR_SHAPE",
-          5: "DMAS_ERR_CUDA", 6: "DMAS_ERR_OOM"}
+          5: "DMAS_ERR_CUDA", 6: "DMAS_ERR_OOM", 7: "DMAS_ERR_NCCL"}
+GATHER = 1 << 16             # sharded plans: gather the images onto the root
+SIGNALS_RESIDENT = 1 << 17   # sharded plans: every rank already holds the signals (no broadcast)
+COMM_ID_BYTES = 128
+XFER_SEND, XFER_RECV, XFER_COPY = 0, 1, 2
 
 
 def RAW(kinds: int) -> int:
@@ -65,6 +69,10 @@ class dmas_plan_desc(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("scratch_bytes", ctypes.c_int64),
         ("bf_engine", ctypes.c_int32),
+        ("n_ranks", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("root", ctypes.c_int32),
+        ("comm_id", ctypes.POINTER(ctypes.c_uint8)),
     ]
 
 
@@ -75,15 +83,22 @@ class dmas_plan_info(ctypes.Structure):
         ("env_decim", ctypes.c_int32), ("device", ctypes.c_int32), ("d_min", ctypes.c_int32),
         ("d_max", ctypes.c_int32), ("psi_tile", ctypes.c_int32), ("t_tile", ctypes.c_int32),
         ("window", ctypes.c_int32), ("chunk_frames", ctypes.c_int32), ("bf_kernel", ctypes.c_int32),
-        ("tile_order", ctypes.c_int32),
+        ("tile_order", ctypes.c_int32), ("n_dirs_total", ctypes.c_int64), ("dir_begin", ctypes.c_int64),
+        ("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("root", ctypes.c_int32), ("sharded", ctypes.c_int32),
     ]
+
+
+class dmas_xfer(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("peer", ctypes.c_int32), ("frame", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("src_elem", ctypes.c_int64), ("dst_elem", ctypes.c_int64),
+                ("count", ctypes.c_int64)]
 
 
 # The exported C symbols (include/dmas.h).  tests/test_abi.py checks the .so exports each.
 EXPORTS = ("dmas_plan_desc_init", "dmas_plan", "dmas_beamform", "dmas_beamform_host", "dmas_delay_table",
            "dmas_delay_fraction",
            "dmas_get_plan_info", "dmas_set_timing", "dmas_timing_read", "dmas_launch_count", "dmas_destroy",
-           "dmas_status_string", "dmas_last_error")
+           "dmas_status_string", "dmas_last_error", "dmas_comm_id", "dmas_shard_range", "dmas_gather_schedule")
 
 
 def _load() -> ctypes.CDLL:
@@ -118,6 +133,15 @@ def _load() -> ctypes.CDLL:
     lib.dmas_status_string.restype = ctypes.c_char_p
     lib.dmas_last_error.argtypes = []
     lib.dmas_last_error.restype = ctypes.c_char_p
+    lib.dmas_comm_id.argtypes = [P]
+    lib.dmas_comm_id.restype = ctypes.c_int
+    lib.dmas_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_int64)]
+    lib.dmas_shard_range.restype = ctypes.c_int
+    lib.dmas_gather_schedule.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_int64, P, ctypes.c_int64,
+                                         ctypes.POINTER(ctypes.c_int64)]
+    lib.dmas_gather_schedule.restype = ctypes.c_int
     return lib
 
 
@@ -131,6 +155,30 @@ def _check(status: int):
 
 def launch_count() -> int:
     return int(lib.dmas_launch_count())
+
+
+def comm_id() -> bytes:
+    """dmas_comm_id: a fresh NCCL unique id (call on one rank, share the bytes with the others)."""
+    buf = (ctypes.c_uint8 * COMM_ID_BYTES)()
+    _check(lib.dmas_comm_id(buf))
+    return bytes(buf)
+
+
+def shard_range(n_dirs: int, n_ranks: int, rank: int):
+    """dmas_shard_range: the contiguous grid rows [g0, g1) `rank` owns."""
+    g0, g1 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.dmas_shard_range(int(n_dirs), int(n_ranks), int(rank), ctypes.byref(g0), ctypes.byref(g1)))
+    return int(g0.value), int(g1.value)
+
+
+def gather_schedule(n_dirs: int, n_ranks: int, rank: int, root: int, n_frames: int, row: int):
+    """dmas_gather_schedule: the transfers `rank` performs to gather one image of an n_frames chunk
+    onto `root`, as a list of dicts (kind, peer, frame, src_elem, dst_elem, count)."""
+    n = ctypes.c_int64()
+    _check(lib.dmas_gather_schedule(n_dirs, n_ranks, rank, root, n_frames, row, None, 0, ctypes.byref(n)))
+    arr = (dmas_xfer * max(1, n.value))()
+    _check(lib.dmas_gather_schedule(n_dirs, n_ranks, rank, root, n_frames, row, arr, n.value, ctypes.byref(n)))
+    return [{f: getattr(arr[i], f) for f, _ in dmas_xfer._fields_ if f != "reserved"} for i in range(n.value)]
 
 
 def _f64(a, shape_last):
@@ -152,7 +200,8 @@ class Plan:
                  max_frames: int = 1, reference_xyz=None, cf_eps: float = 1e-30, lp_taps: int = 127,
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
                  device: int = -1, scratch_bytes: int = 0, env_engine: int = 0,
-                 mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0, bf_engine: int = 0):
+                 mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0, bf_engine: int = 0,
+                 n_ranks: int = 0, rank: int = 0, root: int = 0, comm_id: Optional[bytes] = None):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -184,6 +233,13 @@ class Plan:
             self._keep.append(mf)
             d.mf_taps = self.mf_taps = mf.shape[0]
             d.mf_coeffs = mf.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        if comm_id is not None:
+            if len(comm_id) != COMM_ID_BYTES:
+                raise ValueError(f"comm_id must be {COMM_ID_BYTES} bytes")
+            cid = (ctypes.c_uint8 * COMM_ID_BYTES).from_buffer_copy(comm_id)
+            self._keep.append(cid)
+            d.comm_id = ctypes.cast(cid, ctypes.POINTER(ctypes.c_uint8))
+        d.n_ranks, d.rank, d.root = int(n_ranks), int(rank), int(root)
         self._keep += [mic, dirs]
         _check(lib.dmas_plan(ctypes.byref(d), ctypes.byref(self._h)))
         info = dmas_plan_info()
@@ -193,6 +249,8 @@ class Plan:
         self.n_samples, self.n_out_samples = int(info.n_samples), int(info.n_out_samples)
         self.order, self.max_frames = int(info.order), int(max_frames)
         self.device = int(info.device)
+        self.n_dirs_total, self.dir_begin = int(info.n_dirs_total), int(info.dir_begin)
+        self.sharded, self.rank, self.root = bool(info.sharded), int(info.rank), int(info.root)
 
     # -- dmas_delay_table
     def delay_table(self) -> np.ndarray:
@@ -207,14 +265,17 @@ class Plan:
         return out
 
     def out_shapes(self, n_frames: int, what: int):
+        """(stage, kind, shape) of each output in `outs` order; a sharded plan's shards are
+        [F][n_local][.], gathered images (what & GATHER) [F][n_dirs_total][.] on the root."""
         raw_k, env_k = what & KIND_ALL, (what >> 8) & KIND_ALL
+        rows = self.n_dirs_total if (self.sharded and what & GATHER) else self.n_dirs
         shapes = []
         for name in KIND_ORDER:
             if raw_k & KIND_BITS[name]:
-                shapes.append(("raw", name, (n_frames, self.n_dirs, self.n_samples)))
+                shapes.append(("raw", name, (n_frames, rows, self.n_samples)))
         for name in KIND_ORDER:
             if env_k & KIND_BITS[name]:
-                shapes.append(("env", name, (n_frames, self.n_dirs, self.n_out_samples)))
+                shapes.append(("env", name, (n_frames, rows, self.n_out_samples)))
         return shapes
 
     # -- dmas_beamform (device buffers, async on the current torch stream)
@@ -229,6 +290,12 @@ class Plan:
             raise ValueError(f"signals are on cuda:{signals.device.index}, the plan on cuda:{self.device}")
         F = signals.shape[0]
         shapes = self.out_shapes(F, what)
+        if self.sharded and what & GATHER and self.rank != self.root:
+            # gathered onto the root: this rank computes its shard into plan staging and sends it
+            st = ctypes.c_void_p(stream) if isinstance(stream, int) else (
+                ctypes.c_void_p(stream.cuda_stream) if stream is not None else _current_stream_ptr(self.device))
+            _check(lib.dmas_beamform(self._h, ctypes.c_void_p(signals.data_ptr()), F, None, what, st))
+            return {}
         if outs is None:
             outs = [torch.empty(s, dtype=torch.float32, device=signals.device) for (_, _, s) in shapes]
         if len(outs) != len(shapes):
@@ -245,7 +312,15 @@ class Plan:
         return {(stage, name): o for (stage, name, _), o in zip(shapes, outs)}
 
     # -- dmas_beamform_host (host buffers, synchronous, pipelined copies)
-    def beamform_host(self, signals: np.ndarray, what: int, outs: Optional[list] = None) -> Dict:
+    def beamform_host(self, signals: Optional[np.ndarray], what: int, outs: Optional[list] = None,
+                      n_frames: Optional[int] = None) -> Dict:
+        """Host buffers in and out (synchronous).  Sharded plans: a collective; the root passes the
+        recording and receives the gathered images, the other ranks pass n_frames only."""
+        if self.sharded and self.rank != self.root:
+            _check(lib.dmas_beamform_host(self._h, None, int(n_frames), None, what))
+            return {}
+        if self.sharded:
+            what |= GATHER
         if signals.dtype != np.float32 or not signals.flags.c_contiguous:
             raise TypeError("signals must be C-contiguous float32")
         if signals.ndim != 3 or signals.shape[1:] != (self.n_mics, self.n_samples + max(0, self.mf_taps - 1)):

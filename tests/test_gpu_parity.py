@@ -526,33 +526,34 @@ def test_linear_presteer_with_matched_filter_and_slices(dm):
     assert np.max(np.abs(r - ref)) <= 1e-5 * np.max(np.abs(ref))
 
 
-def test_sharded_beamformer_nccl_single_rank(dm):
-    """parallel.ShardedBeamformer through a real NCCL process group (world size 1 here; the
-    multi-rank host logic is covered with gloo in tests/test_parallel.py): broadcast + beamform +
-    gather reproduce the plain plan bitwise."""
-    import socket
+@pytest.mark.parametrize("what_name", ["env_all", "raw_env_mix"])
+def test_sharded_plan_one_rank_bitwise(dm, what_name):
+    """A one-rank sharded plan (n_ranks = 1 with an NCCL comm id: the exchange code runs on one GPU --
+    the communicator, the in-place ncclBroadcast per chunk, the comm-stream ordering, the gather
+    staging and the gather schedule's local copies) returns images bitwise equal to a plain plan's:
+    resident shards, images gathered onto the root over several double-buffered exchange chunks,
+    and the host-buffer path ("G = 1 vs G > 1 bitwise"; the G > 1 exchange is
+    checked on the CPU by tests/test_parallel.py::test_gather_schedule_assembles_the_image)."""
     import torch
-    import torch.distributed as dist
-    from paper_2511_09165_b200 import parallel
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
-        cfg = gen.config("C2")
-        x = torch.from_numpy(cfg["signals"]).cuda()
-        what = dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS)
-        sb = parallel.ShardedBeamformer(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"])
-        got = sb.beamform(x, what, src=0, gather_to=0)
-        ref = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"]).beamform(x, what)
-        torch.cuda.synchronize()
-        for k in ref:
-            assert torch.equal(got[k], ref[k]), k
-        sb.close()
-    finally:
-        dist.destroy_process_group()
+    cfg = gen.config("C3")
+    sig = np.concatenate([cfg["signals"], gen.random_signals(4, 32, cfg["T"], seed=56)])   # 5 frames
+    x = torch.from_numpy(sig).cuda()
+    what = dm.ENV(dm.KIND_ALL) if what_name == "env_all" else dm.RAW(dm.KIND_CFDMAS) | dm.ENV(dm.KIND_CFDMAS | dm.KIND_DAS)
+    args = (cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 3, cfg["T"])
+    plain = dm.Plan(*args, max_frames=5, scratch_bytes=1)       # 1 frame per chunk (5 envelope-only kinds)
+    ref = {k: v.cpu().numpy() for k, v in plain.beamform(x, what).items()}
+    sp = dm.Plan(*args, max_frames=5, scratch_bytes=1, n_ranks=1, rank=0, root=0, comm_id=dm.comm_id())
+    assert sp.sharded and sp.info["n_dirs_total"] == len(cfg["dirs"]) and sp.info["dir_begin"] == 0
+    assert np.array_equal(sp.delay_table(), plain.delay_table())
+    resident = sp.beamform(x.clone(), what)
+    gathered = sp.beamform(x.clone(), what | dm.GATHER)
+    host = sp.beamform_host(sig, what)
+    torch.cuda.synchronize()
+    for k in ref:
+        assert np.array_equal(resident[k].cpu().numpy(), ref[k]), ("resident", k)
+        assert np.array_equal(gathered[k].cpu().numpy(), ref[k]), ("gathered", k)
+        assert np.array_equal(host[k], ref[k]), ("host", k)
+    sp.close()
 
 
 # ------------------------------------------------------------------ large arrays (microphone-group path)
