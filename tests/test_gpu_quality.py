@@ -110,3 +110,48 @@ def test_beamwidth_falls_with_radius_gpu():
     spread = [max(v for k, v in r.items() if k != "n_mics") - min(v for k, v in r.items() if k != "n_mics")
               for r in rows]
     assert spread[0] > spread[1] > spread[2], spread   # PAPER.md:243 beamwidths converge
+
+
+def test_image_snr_metric_hand_computed():
+    """E_off / image SNR (reading Q20) on a hand-built image: peak 8 at the target
+    (az 0, t 2000); every pixel inside the guard (|az| <= 15 deg AND |t - 2000| <= 1125) is 4 and
+    must be ignored; the 76 rows outside +-15 deg are 0.5 (76 x 4000 pixels) and the 15 rows inside
+    it are 0.25 outside the range guard (15 x 1749 pixels), so after normalising to the peak
+    E_off = (76*4000*0.5 + 15*1749*0.25) / (76*4000 + 15*1749) / 8 and SNR = 20 log10(1 / E_off)."""
+    az = np.arange(-90.0, 91.0, 2.0)
+    T = 4000
+    t = np.arange(T)
+    in_az = np.abs(az) <= 15.0
+    assert in_az.sum() == 15 and (~in_az).sum() == 76
+    env = np.where(in_az[:, None], 0.25, 0.5) * np.ones((1, T))
+    guard = in_az[:, None] & (np.abs(t - 2000)[None, :] <= 1125)
+    assert guard.sum() == 15 * 2251
+    env[guard] = 4.0
+    env[np.argmin(np.abs(az)), 2000] = 8.0
+    e_off = (76 * 4000 * 0.5 + 15 * 1749 * 0.25) / (76 * 4000 + 15 * 1749) / 8.0
+    assert quality.image_snr(env, az, 0.0, 2000) == pytest.approx(20 * math.log10(1.0 / e_off), abs=1e-12)
+    # and the guard really matters: without it the 4.0 plateau raises E_off
+    assert quality.image_snr(env, az, 0.0, 2000, guard_deg=-1.0) < 20 * math.log10(1.0 / e_off) - 1.0
+
+
+@pytest.mark.gpu
+def test_image_snr_gpu_matches_oracle():
+    """Fig. 3 sweep: image SNR of every beamformer, with and without CF, at two
+    input SNRs -- GPU envelope images against the float64 oracle's on the same noisy scenes."""
+    gpu = quality.image_snr_sweep(snrs=(-10.0, 10.0), seeds=(1,))
+    ref = quality.image_snr_sweep(beamform=oracle_beamform, snrs=(-10.0, 10.0), seeds=(1,))
+    for snr in gpu:
+        for k in gpu[snr]:
+            assert gpu[snr][k] == pytest.approx(ref[snr][k], abs=0.01), (snr, k, gpu[snr][k], ref[snr][k])
+
+
+@pytest.mark.gpu
+def test_beamwidth_gpu_matches_oracle():
+    """Fig. 6 sweep: -3 dB beamwidth on 5 mm hexagonal lattices of radius 1 and
+    2 cm, every beamformer with and without CF -- GPU against the oracle's images."""
+    gpu = quality.beamwidth_sweep(radii=(0.01, 0.02))
+    ref = quality.beamwidth_sweep(beamform=oracle_beamform, radii=(0.01, 0.02))
+    for r in gpu:
+        assert gpu[r]["n_mics"] == ref[r]["n_mics"]
+        for k, v in gpu[r].items():
+            assert v == pytest.approx(ref[r][k], abs=1e-3), (r, k, v, ref[r][k])

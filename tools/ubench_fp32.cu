@@ -143,15 +143,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_lds(int stride) {
       const uint32_t a = base + (uint32_t)(c * stride * 8);       // immediate offsets: no address math
       if (W == 4) {
         float v;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
         acc += v;
       } else if (W == 8) {
         float v0, v1;
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v0), "=f"(v1) : "r"(a));
+        asm volatile("ld.volatile.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v0), "=f"(v1) : "r"(a));
         acc += v0 + v1;
       } else {
         float v0, v1, v2, v3;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3) : "r"(a));
+        asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3) : "r"(a));
         acc += (v0 + v1) + (v2 + v3);
       }
     }
