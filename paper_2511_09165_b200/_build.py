@@ -49,15 +49,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
     procs = []
+    headers = [d for d in DEPS if d not in SOURCES]
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj)
+                                                     for d in [src, *headers]):
+            procs.append((obj, None))                          # object up to date
+            continue
         cmd = [nvcc_path(), *flags, "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((obj, subprocess.Popen(cmd)))
     objs = []
     for obj, pr in procs:
-        if pr.wait() != 0:
+        if pr is not None and pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, "nvcc " + obj)
         objs.append(obj)
     tmp = LIB + ".tmp"

@@ -8,7 +8,7 @@
 //   A_q[tau][k] = |y[32 (tau + q) + k]|,  H_q[k][n] = h[n + c - 32 q - k]  (0 outside [0, L)),
 // i.e. per 128-block tile five M=128 x N=32 x K=32 GEMMs.  MACs per output = 160 (127 useful).
 //
-// Precision: 3-pass BF16 split a = a_hi + a_lo, h = h_hi + h_lo; hi*hi + hi*lo + lo*hi with fp32
+// Precision: BF16 split a = a_hi + a_lo, h = h_hi + h_lo; hi*hi + hi*lo + lo*hi with fp32
 // accumulation in TMEM.  BF16 keeps 8 significant bits, so |a - a_hi| <= 2^-8 |a| and the rounded
 // lo part leaves <= 2^-16 |a| (same for h); with the dropped lo*lo term (<= 2^-16) the relative
 // error per product is <= ~3 * 2^-16 ~ 4.6e-5.  The rectified input is >= 0 and all but 34 tiny
@@ -16,11 +16,24 @@
 // inside the 1e-4 parity bar in the worst case (measured: ~2e-6 on C1-C5 images; the adversarial
 // rows of tests/test_gpu_parity.py::test_envelope_tc_adversarial_split_inputs).
 //
-// Why this shape (measured on B200, round-1 microbenchmarks): every tcgen05.mma with N <= 64
-// costs >= 44 cycles, and in SS mode the 4 KB A operand was re-read from shared memory by every
-// MMA, which saturated the SM's L1 data path.  So A lives in TMEM (TS mode: 5 block-shifted copies
-// per split written by tcgen05.st, double-buffered), only the 1 KB H_q operand is read from shared
-// memory, and a tile is 30 MMAs (5 shifts x 2 K-steps x 3 passes).
+// Why this shape (measured on B200): every tcgen05.mma with N <= 64 costs >= 44 cycles, and in SS
+// mode the 4 KB A operand was re-read from shared memory by every MMA.  So A lives in TMEM (TS
+// mode: 5 block-shifted copies per split, double-buffered) and only the H_q operand is read from
+// shared memory.  Per (shift, K-step) two MMAs: D[0:64] += A_hi x [H_hi | H_lo] (N = 64) and
+// D[0:32] += A_lo x H_hi (N = 32), 20 per tile; the epilogue adds D[0:32] + D[32:64].
+//
+// The block-shifted A copies: the converted tile is stored "column-chunk major" -- 16-byte chunk j
+// of every block row r at j * CLBO + 16 r -- so rows are 16 B apart everywhere and the canonical
+// no-swizzle K-major layout (SBO = 128 B per 8 rows) describes the tile starting at ANY row.
+// Shift 0 is copied into TMEM by the tensor core itself (tcgen05.cp 128x256b through a descriptor
+// whose start moves by q rows, issued by the MMA thread ahead of its MMAs: same-thread tcgen05.cp
+// and tcgen05.mma execute in issue order); shifts 1..4 by 4 copy warps (LDS.128 + tcgen05.st).
+// Measured per 16-frame C5 chunk (tools/time_variants.py, profiles/r02/envelope_variants.json):
+// all 5 shifts by copy warps 1.63 ms, 1 by tcgen05.cp 1.58 ms, 2: 1.64, 3: 1.72, all 5: 2.21
+// (tcgen05.cp moves ~40 B/clk/SM and queues in front of the MMAs).  The converters load their
+// whole share of a stage before converting (round 1 converted item by item: the converter warps
+// were ~85% busy on load latency).  Role profile after both changes (DMAS_TC_PROFILE): MMA issuer
+// ~75% busy, epilogue ~75%, converters ~60%, copy warps ~55%; HBM at ~0.85 of the copy bandwidth.
 //
 // Data movement: 3D TMA tensor maps view a [rows][T] image as [rows][T/32 blocks][32 samples]
 // with 128-byte swizzle.  The load box is 132 blocks (the tile + a 2-block halo each side; blocks
@@ -29,11 +42,12 @@
 //
 // Per CTA (persistent, 1 CTA / SM, warp-specialised roles linked by mbarriers, every stage
 // double- or quad-buffered so the roles run concurrently):
+//   warps 0..3      epilogue: tcgen05.ld (2 x 32 columns) -> add -> clamp -> swizzled smem -> TMA store
+//   warps 4..7      copy: block shifts 1..4 of each TMEM lane quarter (LDS.128 + tcgen05.st.x16)
+//   warps 8..15     converters: stage -> |.| -> BF16 hi / lo, once per sample, column-chunk major
+//   warp 16         MMA issuer (one elected lane): 4 tcgen05.cp (shift 0) + 20 tcgen05.mma per tile
+//                   into one of two TMEM accumulators
 //   warp 17 lane 0  TMA producer: 4-slot ring of input tiles
-//   warps 8..15     converters: stage -> |.| -> BF16 hi / lo, once per sample, into a swizzled buffer
-//   warps 0..3      copy: the 5 block-shifted A copies of each TMEM lane (tcgen05.st.x16), hi and lo
-//   warp 16 lane 0  MMA issuer: 30 tcgen05.mma per tile into one of two TMEM accumulators
-//   warps 4..7      epilogue: tcgen05.ld.x32 -> clamp -> swizzled smem -> TMA tensor store
 
 #include <cstdint>
 #include <cuda.h>
@@ -61,36 +75,62 @@ constexpr int NSTAGE = DMAS_TC_NSTAGE;
 #define DMAS_TC_NOUT 4
 #endif
 constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (TMA stores in flight)
+// block shifts copied into TMEM by tcgen05.cp (shifts 0 .. NCP-1); the others by the copy warps
+#ifndef DMAS_TC_NCP
+#define DMAS_TC_NCP 1
+#endif
+constexpr int NCP = DMAS_TC_NCP;
+static_assert(NCP >= 0 && NCP <= 5, "NCP");
+constexpr int NCOPYW = NCP < 5 ? 4 : 0;            // copy warps (one TMEM lane quarter each)
+// epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, 16 output columns each)
+#ifndef DMAS_TC_EPIW
+#define DMAS_TC_EPIW 4
+#endif
+constexpr int EPIW = DMAS_TC_EPIW;
+static_assert(EPIW == 4 || EPIW == 8, "EPIW");
+constexpr int EPI_COLS = BLK * 4 / EPIW;            // output columns per epilogue thread (32 or 16)
 // warp roles
-constexpr int COPY_WARP0 = 0;                       // warps 0..3: shifted A copies -> TMEM (lane quarter = warp)
-constexpr int EPI_WARP0 = 4;                        // warps 4..7: TMEM accumulator -> clamp -> TMA store
-constexpr int CONV_WARP0 = 8;                       // warps 8..15: fp32 stage -> bf16 hi / lo buffer
+constexpr int EPI_WARP0 = 0;                        // TMEM accumulator -> clamp -> TMA store
+constexpr int COPY_WARP0 = EPIW;                    // the other shifted A copies (LDS + tcgen05.st)
+constexpr int CONV_WARP0 = COPY_WARP0 + NCOPYW;     // 8 warps: fp32 stage -> bf16 hi / lo buffer
 constexpr int CONV_WARPS = 8;
-constexpr int MMA_WARP = 16;
-constexpr int TMA_WARP = 17;
+constexpr int MMA_WARP = CONV_WARP0 + CONV_WARPS;
+constexpr int TMA_WARP = MMA_WARP + 1;
 constexpr int CONV_THREADS = CONV_WARPS * 32;
-constexpr int THREADS = 18 * 32;
+constexpr int THREADS = (TMA_WARP + 1) * 32;
 
-// H_q^T in shared memory: K-major canonical layout, no swizzle, 8 bf16 per 16-byte core row.
-constexpr int B_LBO = BLK * 16;                     // 512 B between K core columns
-constexpr int B_BYTES = B_LBO * (BLK / 8);          // 2048 B per (shift, split)
+// H_q^T in shared memory: K-major canonical layout, no swizzle, 8 bf16 per 16-byte core row; per
+// shift q the N rows are [H_q hi (32 rows) | H_q lo (32 rows)], so one N = 64 MMA multiplies A_hi by
+// both halves of the split taps and an N = 32 MMA on the first 32 rows multiplies A_lo by H_hi:
+// 2 MMAs per (shift, K-step) instead of 3 (the instruction issue -- ~44 cycles per tcgen05.mma at
+// N <= 64 -- bounds the tile, ncu/role profile DESIGN.md §6).
+constexpr int BROWS = 2 * BLK;                      // 64 B-operand rows per shift
+constexpr int B_LBO = BROWS * 16;                   // 1024 B between K core columns
+constexpr int B_BYTES = B_LBO * (BLK / 8);          // 4096 B per shift
 constexpr int K_MMA = 16;
 
 // TMEM columns (fp32 / packed bf16x2): A copies [buf][split][shift] x 16 columns, then D[buf].
 constexpr int A_COLS = 16;                          // 32 bf16 of one block row
 constexpr int A_BUF_COLS = 2 * NQ * A_COLS;         // 160
-constexpr int D_COL0 = 2 * A_BUF_COLS;              // 320
+constexpr int D_COL0 = 2 * A_BUF_COLS;              // 320: D[buf] = 64 columns (hi*h_hi + lo*h_hi | hi*h_lo)
+constexpr int D_COLS = 2 * BLK;
+static_assert(D_COL0 + 2 * D_COLS <= 512, "TMEM columns");
 constexpr int TMEM_COLS = 512;
 
-constexpr int CONV_BYTES = STAGE_BYTES;             // [132 rows][64 B bf16 hi | 64 B bf16 lo], swizzled
+// converted tile, column-chunk major: chunk j (0..3 hi, 4..7 lo; 8 bf16 = samples 8(j%4)..+7 of the
+// block) of block row r (block -2 + r) at j * CLBO + 16 r.  CLBO = 132 rows * 16 B.
+constexpr int CLBO = IN_BLOCKS * 16 + 96;           // 2208 B between chunk columns (== 32 mod 128: a
+                                                    // converter half-warp's 4 chunk stores hit disjoint banks)
+constexpr int CONV_BYTES = (8 * CLBO + 1023) / 1024 * 1024;   // 18432 B (keeps the staging below 1024-aligned)
 constexpr int OFF_STAGE = 0;
 constexpr int OFF_CONV = OFF_STAGE + NSTAGE * STAGE_BYTES;
 constexpr int OFF_OUT = OFF_CONV + 2 * CONV_BYTES;
 constexpr int OFF_B = OFF_OUT + NOUT * OUT_BYTES;
-constexpr int SMEM_BYTES = OFF_B + 2 * NQ * B_BYTES + 1024;   // + alignment slack
+constexpr int SMEM_BYTES = OFF_B + NQ * B_BYTES + 1024;   // + alignment slack
 
-// instruction descriptor: D f32, A/B bf16 (kind::f16), K-major, N = 32, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BLK >> 3) << 17) | ((128u >> 4) << 24);
+// instruction descriptors: D f32, A/B bf16 (kind::f16), K-major, M = 128, N = 32 / 64
+constexpr uint32_t idesc(uint32_t n) { return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24); }
+constexpr uint32_t IDESC32 = idesc(BLK), IDESC64 = idesc(2 * BLK);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -123,7 +163,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 #ifdef DMAS_TC_PROFILE
-__device__ unsigned long long g_tc_prof[148][8];
+// per SM: [role][0] = wait on the role's input barrier, [role][1] = wait on its output-free barrier,
+// [5][0] = the MMA warp's total cycles; roles 0 TMA, 1 MMA, 2 converter (warp 0 of the role), 3 epilogue, 4 copy
+__device__ unsigned long long g_tc_prof[148][6][2];
 #define PROF_WAIT(slot, expr)                          \
   do {                                                 \
     const unsigned long long t0_ = clock64();          \
@@ -152,15 +194,21 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1 << 46);
 }
-__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc_v,
+                                       uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(IDESC), "r"(accumulate));
+      "r"(a_tmem), "l"(b), "r"(idesc_v), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+// smem -> TMEM copy by the tensor core: 128 rows (lanes) x 256 bits (8 columns) from the matrix
+// the descriptor describes; asynchronous, ordered with this thread's tcgen05.mma
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
 }
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
@@ -188,6 +236,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]) {
+  if constexpr (N == 32) tmem_ld32(taddr, v);
+  else tmem_ld16(taddr, v);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];
@@ -264,10 +328,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&conv_full[b], CONV_THREADS);
-      mbar_init(&conv_empty[b], 128);
-      mbar_init(&a_full[b], 128);
+      mbar_init(&conv_empty[b], 1 + 32 * NCOPYW);    // copy warps' reads + the commit after the cps
+      mbar_init(&a_full[b], 32 * NCOPYW > 0 ? 32 * NCOPYW : 1);
       mbar_init(&mma_done[b], 1);
-      mbar_init(&d_empty[b], 128);
+      mbar_init(&d_empty[b], 32 * EPIW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -283,8 +347,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     uint32_t hi = 0, lo = 0;
     if (j >= 0 && j < L) split_bf16(taps.h[j], hi, lo);
     const uint32_t off = (uint32_t)(qi * B_BYTES + n * 16 + (k >> 3) * B_LBO + (k & 7) * 2);
-    *reinterpret_cast<uint16_t*>(smem + OFF_B + off) = (uint16_t)hi;
-    *reinterpret_cast<uint16_t*>(smem + OFF_B + NQ * B_BYTES + off) = (uint16_t)lo;
+    *reinterpret_cast<uint16_t*>(smem + OFF_B + off) = (uint16_t)hi;                 // row n
+    *reinterpret_cast<uint16_t*>(smem + OFF_B + off + BLK * 16) = (uint16_t)lo;      // row 32 + n
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -314,84 +378,46 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int buf = (int)(jj & 1);
-      PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
+      PROF_WAIT(0, mbar_wait(&conv_full[buf], (uint32_t)((jj >> 1) & 1)));
+      if (NCOPYW) PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
       if (jj >= 2) PROF_WAIT(1, mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * BLK);
+      const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * D_COLS);
       const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
       uint32_t is_leader;
       asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(is_leader));
       if (is_leader) {
+        // the block-shifted A copies: TMEM lane tau, columns [split][shift q][16] <- converted block
+        // row tau + q (rows 16 B apart, so the descriptor of row q is the base + 16 q); two
+        // 128x256b copies (chunks 0-1, 2-3 of the split) per (split, shift).  A[buf] was last read
+        // by tile jj - 2's MMAs, which precede these copies in this thread's tcgen05 pipeline.
+        const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
 #pragma unroll
-        for (int pass = 0; pass < 3; ++pass) {             // lo*hi, hi*lo, hi*hi
-          const uint32_t a_split = (pass == 0) ? (uint32_t)(NQ * A_COLS) : 0u;
-          const uint64_t b_split = (pass == 1) ? (uint64_t)((NQ * B_BYTES) >> 4) : 0;
+        for (int split = 0; split < 2; ++split)
 #pragma unroll
-          for (int qi = 0; qi < NQ; ++qi) {
+          for (int qi = 0; qi < NCP; ++qi)
 #pragma unroll
-            for (int s = 0; s < BLK / K_MMA; ++s)
-              mma_ts(d, a0 + a_split + (uint32_t)(qi * A_COLS + s * (K_MMA / 2)),
-                     b0 + b_split + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4), (pass | qi | s) ? 1u : 0u);
+            for (int half = 0; half < 2; ++half)
+              tmem_cp_128x256b(a0 + (uint32_t)(split * NQ * A_COLS + qi * A_COLS + half * 8),
+                               smem_desc(cv + (uint32_t)((split * 4 + half * 2) * CLBO + qi * 16), CLBO, 128));
+        // per (shift, K-step): D[0:64] += A_hi x [H_hi | H_lo] (N = 64), D[0:32] += A_lo x H_hi (N = 32)
+#pragma unroll
+        for (int qi = 0; qi < NQ; ++qi) {
+#pragma unroll
+          for (int s = 0; s < BLK / K_MMA; ++s) {
+            const uint64_t b = b0 + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4);
+            const uint32_t a = a0 + (uint32_t)(qi * A_COLS + s * (K_MMA / 2));
+            mma_ts(d, a, b, IDESC64, (qi | s) ? 1u : 0u);
+            mma_ts(d, a + (uint32_t)(NQ * A_COLS), b, IDESC32, 1u);
           }
         }
         mma_commit(&mma_done[buf]);
+        mma_commit(&conv_empty[buf]);                   // the cps are done with the smem tile
       }
       __syncwarp();
     }
-  } else if (warp >= CONV_WARP0) {
-    // ================= converters: staged fp32 tile -> |.| -> bf16 hi / lo, once per sample;
-    // conv row r = block -2 + r, chunks 0..3 hi, 4..7 lo (128-byte swizzle)
-    const int ct = tid - CONV_WARP0 * 32;
-    for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int slot = (int)(jj % NSTAGE), buf = (int)(jj & 1);
-      PROF_WAIT(0, mbar_wait(&stage_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
-      if (jj >= 2) PROF_WAIT(1, mbar_wait(&conv_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
-      const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
-      const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
-      for (int i = ct; i < IN_BLOCKS * 8; i += CONV_THREADS) {       // i = (row, fp32 chunk f)
-        const int r = i >> 3, f = i & 7;
-        const float4 v = lds128(st + swz(r, f));
-        uint32_t h01, l01, h23, l23;
-        split2(fabsf(v.x), fabsf(v.y), h01, l01);
-        split2(fabsf(v.z), fabsf(v.w), h23, l23);
-        const uint32_t half = (uint32_t)(f & 1) * 8;
-        sts64(cv + swz(r, f >> 1) + half, h01, h23);
-        sts64(cv + swz(r, 4 + (f >> 1)) + half, l01, l23);
-      }
-      mbar_arrive(&stage_empty[slot]);
-      mbar_arrive(&conv_full[buf]);
-    }
-  } else if (warp >= EPI_WARP0) {
-    // ================= epilogue: TMEM accumulator -> clamp -> swizzled smem -> TMA store
-    const int quarter = warp - EPI_WARP0;
-    const int tau = 32 * quarter + lane;
-    const int et = tid - EPI_WARP0 * 32;
-    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
-    for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int buf = (int)(jj & 1), ob = (int)(jj % NOUT);
-      PROF_WAIT(0, mbar_wait(&mma_done[buf], (uint32_t)((jj >> 1) & 1)));
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[32];
-      tmem_ld32(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * BLK), v);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&d_empty[buf]);
-      if (et == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
-      named_bar(1, 128);
-      const uint32_t osa = smem_u32(smem + OFF_OUT + ob * OUT_BYTES);
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        sts128(osa + swz(tau, cc), make_float4(fmaxf(v[4 * cc], 0.f), fmaxf(v[4 * cc + 1], 0.f),
-                                               fmaxf(v[4 * cc + 2], 0.f), fmaxf(v[4 * cc + 3], 0.f)));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 128);
-      if (et == 0) {
-        tma_store_3d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)tile_row(jj));
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  } else {
-    // ================= copy warps: the 5 block-shifted copies of TMEM lane tau (hi and lo)
+  } else if (warp >= COPY_WARP0 && warp < COPY_WARP0 + NCOPYW) {
+    // ================= copy warps: shifts NCP..4 of TMEM lane tau (hi and lo), LDS.128 + tcgen05.st
     const int quarter = warp - COPY_WARP0;
     const int tau = 32 * quarter + lane;
     const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
@@ -403,13 +429,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
       const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS);
 #pragma unroll
-      for (int qi = 0; qi < NQ; ++qi) {
-        const int r = tau + qi;                            // conv row of block tau + q (row 0 = block -2)
+      for (int qi = NCP; qi < NQ; ++qi) {
+        const uint32_t row = cv + (uint32_t)((tau + qi) * 16);          // block row tau + q
         uint4 hv[4], lv[4];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          hv[g] = lds128u(cv + swz(r, g));
-          lv[g] = lds128u(cv + swz(r, 4 + g));
+          hv[g] = lds128u(row + (uint32_t)(g * CLBO));
+          lv[g] = lds128u(row + (uint32_t)((4 + g) * CLBO));
         }
         tmem_st16(a_col + (uint32_t)(qi * A_COLS), hv);
         tmem_st16(a_col + (uint32_t)(NQ * A_COLS + qi * A_COLS), lv);
@@ -419,15 +445,89 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&a_full[buf]);
     }
+  } else if (warp >= CONV_WARP0 && warp < CONV_WARP0 + CONV_WARPS) {
+    // ================= converters: staged fp32 tile -> |.| -> bf16 hi / lo, once per sample;
+    // block row r = block -2 + r; hi chunk j at j * CLBO + 16 r, lo chunk j at (4 + j) * CLBO + 16 r
+    const int ct = tid - CONV_WARP0 * 32;
+    for (int64_t jj = 0; jj < my_tiles; ++jj) {
+      const int slot = (int)(jj % NSTAGE), buf = (int)(jj & 1);
+      PROF_WAIT(0, mbar_wait(&stage_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
+      if (jj >= 2) PROF_WAIT(1, mbar_wait(&conv_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
+      const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
+      const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
+      // items i = (row, fp32 chunk f) = ct + 256 k: every load of the thread first, then the
+      // splits and stores (the loads' latency overlaps instead of adding up item by item)
+      constexpr int NIT = (IN_BLOCKS * 8 + CONV_THREADS - 1) / CONV_THREADS;   // 5 (the last partial)
+      float4 v[NIT];
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int i = ct + k * CONV_THREADS;
+        if (i < IN_BLOCKS * 8) v[k] = lds128(st + swz(i >> 3, i & 7));
+      }
+      mbar_arrive(&stage_empty[slot]);                 // the stage is in registers: TMA may refill it
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int i = ct + k * CONV_THREADS;
+        if (i >= IN_BLOCKS * 8) break;
+        const int r = i >> 3, f = i & 7;
+        uint32_t h01, l01, h23, l23;
+        split2(fabsf(v[k].x), fabsf(v[k].y), h01, l01);
+        split2(fabsf(v[k].z), fabsf(v[k].w), h23, l23);
+        const uint32_t off = (uint32_t)((f >> 1) * CLBO + r * 16 + (f & 1) * 8);
+        sts64(cv + off, h01, h23);
+        sts64(cv + off + 4 * CLBO, l01, l23);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05.cp
+      mbar_arrive(&conv_full[buf]);
+    }
+  } else if (warp < EPI_WARP0 + EPIW) {
+    // ================= epilogue: TMEM accumulator -> clamp -> swizzled smem -> TMA store; thread =
+    // (block row tau, EPI_COLS of its 32 outputs)
+    const int quarter = (warp - EPI_WARP0) & 3, part = (warp - EPI_WARP0) >> 2;
+    const int tau = 32 * quarter + lane;
+    const int et = tid - EPI_WARP0 * 32;
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    const uint32_t col0 = (uint32_t)(part * EPI_COLS);
+    for (int64_t jj = 0; jj < my_tiles; ++jj) {
+      const int buf = (int)(jj & 1), ob = (int)(jj % NOUT);
+      PROF_WAIT(0, mbar_wait(&mma_done[buf], (uint32_t)((jj >> 1) & 1)));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float v[EPI_COLS];
+      {
+        float w[EPI_COLS];                             // (hi + lo) * h_hi  +  hi * h_lo
+        tmem_ld_cols<EPI_COLS>(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS) + col0, v);
+        tmem_ld_cols<EPI_COLS>(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS + BLK) + col0, w);
+#pragma unroll
+        for (int i = 0; i < EPI_COLS; ++i) v[i] = __fadd_rn(v[i], w[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&d_empty[buf]);
+      if (et == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
+      named_bar(1, 32 * EPIW);
+      const uint32_t osa = smem_u32(smem + OFF_OUT + ob * OUT_BYTES);
+#pragma unroll
+      for (int cc = 0; cc < EPI_COLS / 4; ++cc)
+        sts128(osa + swz(tau, (int)(col0 / 4) + cc),
+               make_float4(fmaxf(v[4 * cc], 0.f), fmaxf(v[4 * cc + 1], 0.f), fmaxf(v[4 * cc + 2], 0.f),
+                           fmaxf(v[4 * cc + 3], 0.f)));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar(1, 32 * EPIW);
+      if (et == 0) {
+        tma_store_3d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)tile_row(jj));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 #ifdef DMAS_TC_PROFILE
   if (lane == 0 && blockIdx.x < 148) {
     const int role = warp == TMA_WARP ? 0 : warp == MMA_WARP ? 1 : warp == CONV_WARP0 ? 2 : warp == EPI_WARP0 ? 3
-                   : warp == COPY_WARP0 ? 4 : -1;
-    if (role == 1) g_tc_prof[blockIdx.x][7] = clock64() - t_start;
-    if (role >= 0) { g_tc_prof[blockIdx.x][role] = prof[0]; if (role >= 1) g_tc_prof[blockIdx.x][role + 1 > 6 ? 6 : role + 1] += 0; }
-    if (role == 1) g_tc_prof[blockIdx.x][5] = prof[1];   // mma: d_empty wait
-    if (role == 2) g_tc_prof[blockIdx.x][6] = prof[1];   // conv: conv_empty wait
+                   : (NCOPYW && warp == COPY_WARP0) ? 4 : -1;
+    if (role >= 0) {
+      g_tc_prof[blockIdx.x][role][0] = prof[0];
+      g_tc_prof[blockIdx.x][role][1] = prof[1];
+    }
+    if (role == 1) g_tc_prof[blockIdx.x][5][0] = clock64() - t_start;
     (void)my_tiles;
   }
 #endif

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_quality.py -m gpu -x -q -rA > gpurun_out/pytest_quality.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_quality.log
-python tools/ubench.py r02 > gpurun_out/ubench.log 2>&1; echo "ubench rc=$?" >> gpurun_out/ubench.log
-python bench.py --workload C4 --steps 5 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+B=paper_2511_09165_b200/build
+timeout 900 python tools/time_variants.py $B/libdmas_e4.so $B/libdmas_e8.so $B/libdmas_e8n0.so $B/libdmas_e8n2.so $B/libdmas_e8p.so > gpurun_out/variants_e.log 2>&1
 echo done
