@@ -56,6 +56,7 @@ PHI_P = {2: 5, 3: 6, 4: 9, 5: 10}
 OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
 OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
 BF_KERNELS = {0: "k_beamform", 1: "k_beamform_lds64", 2: "k_beamform_mg"}   # dmas_plan_info.bf_kernel
+SURVEY_F2_CEILING = {"C5": 131e9 / 1e9, "C4": 73e9 / 1e9}    # SURVEY.md §8(d) model ceilings, Gpx/s per GPU
 ENV_PRECISION = ("tcgen05 low-pass, 3-pass BF16 split: <= 3 * 2^-16 ~ 4.6e-5 of the envelope value (bound); "
                  "the FP32 FIR (env_engine = 1) is timed in all_fp32")
 
@@ -78,7 +79,7 @@ def parse():
                     help="linear-interpolation pre-steering (fractional delays, roots on the fly; NEXT-2)")
     ap.add_argument("--raw", action="store_true",
                     help="raw recordings in: the step includes the GPU matched filter (paper Fig. 1 pipeline)")
-    ap.add_argument("--e2e-frames", type=int, default=16)
+    ap.add_argument("--e2e-frames", type=int, default=0, help="frames per e2e step (0: the whole step)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -459,6 +460,12 @@ def run_ours(args, rank, world, local):
         "peak_basis": (f"{FP32_LANES_PER_SM_CLK} FP32 lanes/clk/SM x 2 x {sm_count} SMs x {sm_max:.0f} MHz "
                        "(guide unit counts at the max SM clock; tools/ubench_fp32.cu measures lanes/clk, "
                        "profiles/r02/ubench.json)"),
+        "step_s8d": {"flop_per_px": flop_px + 2 * LP_TAPS, "TFLOP_s": (flop_px + 2 * LP_TAPS) * value / 1e12,
+                     "frac": (flop_px + 2 * LP_TAPS) * value / 1e12 / (flop_peak * world),
+                     "model_ceiling_gpx_s": SURVEY_F2_CEILING.get(args.workload),
+                     "note": "SURVEY.md §8(d) whole-step count N_m*phi_p + 30 + 254 per enveloped image (the "
+                             "127-tap low-pass as FP32 FMAs, although it runs on the tensor cores) against the "
+                             "FP32 peak of all GPUs; model_ceiling = the §8(d) F2 ceiling of the step (Gpx/s, 1 GPU)"},
         "issue": {"lane_ops_per_px": ops_px, "T_lane_ops_s": ach_ops, "frac_of_lane_peak": ach_ops / lane_peak,
                   "formulation_flop_ceiling": PHI_P[p] / (2.0 * OPS_PER_MIC[p]),
                   "ncu_fma_pipe_pct": pb.get("pipe_fma_pct"), "ncu_issue_active_pct": pb.get("issue_active_pct"),
@@ -497,11 +504,21 @@ def run_ours(args, rank, world, local):
     # ---- end to end through the public API with host buffers (pinned), copies in the timed region
     e2e = None
     if not args.no_e2e and not args.raw:
-        Fe = min(args.e2e_frames, F)
+        Fe = min(args.e2e_frames or F, F)
         host_io = rank == 0 or not sharded
         if host_io:
-            hsig = torch.from_numpy(np.ascontiguousarray(cfg["signals"][:Fe])).pin_memory()
-            hout = torch.empty((Fe, n_dirs_total if sharded else plan.n_dirs, T), dtype=torch.float32).pin_memory()
+            rows_h = n_dirs_total if sharded else plan.n_dirs
+            try:                                          # the whole step: 64 GiB of pinned images for C5
+                hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
+            except RuntimeError:
+                Fe = min(16, F)
+                hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
+            hsig = torch.empty((Fe,) + cfg["signals"].shape[1:], dtype=torch.float32, pin_memory=True)
+            hsig.copy_(torch.from_numpy(cfg["signals"][:Fe]))
+        if world > 1:                                     # every rank takes part with the root's Fe
+            t = torch.tensor([Fe], device=dev)
+            dist.broadcast(t, src=0)
+            Fe = int(t.item())
 
         def call_host():
             if host_io:
