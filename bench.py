@@ -40,6 +40,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")     # NCCL's version banner would precede the JSON line on stdout
 
 import numpy as np  # noqa: E402
 
@@ -86,6 +87,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip all_fp32 / linearity / C1 latency")
     ap.add_argument("--cpu-dirs", type=int, default=0, help="directions per core in the all-core CPU sample (0 = all)")
     ap.add_argument("--dry-run", action="store_true", help="CPU only: spawn ranks, shard the grid, print the line")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use a sharded plan (NCCL communicator, broadcast, gather) even on one GPU: exercises "
+                         "the multi-GPU code path of this script and the library where only one GPU is available")
     return ap.parse_args()
 
 
@@ -350,7 +354,7 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    sharded = args.mode == "dirshard" and world > 1
+    sharded = args.mode == "dirshard" and (world > 1 or args.force_sharded)
 
     # ---- inputs (resident in HBM before the timed region)
     F = args.frames

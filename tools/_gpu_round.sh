@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-S=$(date +%s); python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r2d.json 2> gpurun_out/bench_r2d.err; echo "bench rc=$? wall=$(( $(date +%s) - S ))s" >> gpurun_out/bench_r2d.err
+timeout 900 python bench.py --steps 3 --warmup 2 --force-sharded --no-cpu-baseline --no-extras --e2e-frames 32 > gpurun_out/bench_sharded1.json 2> gpurun_out/bench_sharded1.err; echo "rc=$?" >> gpurun_out/bench_sharded1.err
 echo done
