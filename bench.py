@@ -40,7 +40,6 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")     # NCCL's version banner would precede the JSON line on stdout
 
 import numpy as np  # noqa: E402
 
@@ -98,6 +97,15 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+_OUT = sys.stdout
+
+
+def emit(line: dict):
+    """The one JSON line of the run, on the real stdout."""
+    _OUT.write(json.dumps(line) + "\n")
+    _OUT.flush()
 
 
 def free_port() -> int:
@@ -227,7 +235,7 @@ def run_reference(args, rank, world):
         "note": "ms_per_step is the measured time of one sample step (one frame, all directions); value is px/s "
                 "of that sample, the same metric and unit as the GPU arm",
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -333,8 +341,8 @@ def run_dry(args, rank, world):
     else:
         seen = [info]
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
-                          "ranks": seen, "config": config_dict(args, world)}), flush=True)
+        emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+                          "ranks": seen, "config": config_dict(args, world)})
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -573,7 +581,7 @@ def run_ours(args, rank, world, local):
         if gathered:
             line["gathered"] = gathered
         line.update(extras)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if sharded:
         sb.close()
     else:
@@ -665,6 +673,12 @@ def main():
     if world != args.gpus:
         print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
         return 2
+    # stdout carries exactly one JSON line: anything else written to fd 1 (NCCL's version banner when
+    # NCCL_DEBUG=VERSION, library messages) goes to stderr; emit() writes to the saved real stdout
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.dry_run:
         return run_dry(args, rank, world)
     if args.impl == "reference":
