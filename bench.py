@@ -517,26 +517,29 @@ def run_ours(args, rank, world, local):
     e2e = None
     if not args.no_e2e and not args.raw:
         Fe = min(args.e2e_frames or F, F)
-        host_io = rank == 0 or not sharded
-        if host_io:
-            rows_h = n_dirs_total if sharded else plan.n_dirs
-            try:                                          # the whole step: 64 GiB of pinned images for C5
-                hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
-            except RuntimeError:
-                Fe = min(16, F)
-                hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
+        # every rank lands its own image rows in host memory (sharded: its shard, copied over its
+        # own PCIe link; the root's recording comes in and is broadcast on the device)
+        rows_h = plan.n_dirs
+        try:                                              # the whole step: 64 GiB of pinned images for C5
+            hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
+        except RuntimeError:
+            Fe = min(16, F)
+            hout = torch.empty((Fe, rows_h, T), dtype=torch.float32, pin_memory=True)
+        if world > 1:                                     # every rank takes the smallest Fe
+            t = torch.tensor([Fe], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            Fe = int(t.item())
+            hout = hout[:Fe]
+        hsig = None
+        if rank == 0 or not sharded:
             hsig = torch.empty((Fe,) + cfg["signals"].shape[1:], dtype=torch.float32, pin_memory=True)
             hsig.copy_(torch.from_numpy(cfg["signals"][:Fe]))
-        if world > 1:                                     # every rank takes part with the root's Fe
-            t = torch.tensor([Fe], device=dev)
-            dist.broadcast(t, src=0)
-            Fe = int(t.item())
 
         def call_host():
-            if host_io:
+            if hsig is not None:
                 plan.beamform_host(hsig.numpy(), what, outs=[hout.numpy()])
             else:
-                plan.beamform_host(None, what, n_frames=Fe)
+                plan.beamform_host(None, what, outs=[hout.numpy()], n_frames=Fe)
 
         call_host()                                   # warm-up (allocates the staging)
         times = []
@@ -555,9 +558,10 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(Fe * n_mics * T * 4) * (world if args.mode == "weak" else 1),
                "d2h_bytes_per_step": int(e_px * 4), "frames_per_step": Fe,
                "ratio_to_device_value": (e_px / et) / value,
-               "timing": "host wall clock around the synchronous dmas_beamform_host call (pinned host buffers; "
-                         "H2D, kernels and D2H pipelined in chunks; sharded: the root's buffers, images gathered "
-                         "onto the root); bound by the PCIe device-to-host copy of fp32 images"}
+               "timing": "host wall clock around the synchronous dmas_beamform_host call, max over ranks (pinned "
+                         "host buffers; H2D, kernels and D2H pipelined in chunks; sharded: the root's recording in, "
+                         "broadcast on the device, every rank's image shard out over its own PCIe link); bound by "
+                         "the PCIe device-to-host copy of fp32 images"}
 
     # ---- extras on one GPU: all-FP32 step, linearity in N_psi, C1 launch latency
     extras = {}

@@ -174,7 +174,11 @@ dmas_status dmas_beamform(dmas_plan_t plan, const float* signals, int32_t n_fram
    pipelined in frame chunks over copy and compute streams; synchronous (returns when every
    output is in host memory).  Host buffers may be pageable, but only page-locked buffers
    (cudaHostAlloc / cudaHostRegister) overlap copies with compute.  Any n_frames >= 0 is
-   accepted (not bounded by max_frames). */
+   accepted (not bounded by max_frames).
+   Sharded plans (a collective): the root's host_signals go in (NULL elsewhere) and are broadcast
+   on the device; with DMAS_GATHER in `what` the images are gathered onto the root and land in the
+   root's host_outs (full [F][n_dirs][.]; NULL elsewhere); without it every rank copies its own
+   shard [F][n_local][.] into its own host_outs, in parallel over the ranks' PCIe links. */
 dmas_status dmas_beamform_host(dmas_plan_t plan, const float* host_signals, int32_t n_frames,
                                float* const* host_outs, uint32_t what);
 

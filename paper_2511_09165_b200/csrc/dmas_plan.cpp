@@ -1012,29 +1012,39 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
   dmas_status st = check_what(p, what, raw_k, env_k);
   if (st != DMAS_OK) return st;
   if (n_frames == 0) return DMAS_OK;
-  // sharded plans: the root's host buffers go in and come out; the exchange is the device path's
-  // (broadcast of the root's signals, images gathered onto the root); other ranks pass NULL
-  const bool host_io = p->comm == nullptr || p->rank == p->root;
+  // sharded plans: the root's host signals go in (broadcast on the device); with DMAS_GATHER the
+  // images are gathered onto the root and come out into the root's host buffers (the other ranks
+  // pass NULL outputs), without it every rank copies its own shard into its own host buffers
+  const bool sharded = p->comm != nullptr;
+  const bool gather = sharded && (what & DMAS_GATHER);
+  const bool h2d = !sharded || p->rank == p->root;
+  const bool d2h = !sharded || !gather || p->rank == p->root;
   const int n_out = popcount5(raw_k) + popcount5(env_k);
-  if (host_io) {
-    if (!host_signals || !host_outs) return fail(DMAS_ERR_NULL, "host buffer is NULL");
+  if (h2d && !host_signals) return fail(DMAS_ERR_NULL, "host signals are NULL");
+  if (d2h) {
+    if (!host_outs) return fail(DMAS_ERR_NULL, "host outputs are NULL");
     for (int i = 0; i < n_out; ++i)
       if (!host_outs[i]) return fail(DMAS_ERR_NULL, "output pointer is NULL");
   }
   std::lock_guard<std::mutex> lk(p->mu);
   DeviceGuard guard(p->device);
 
-  // frames per pipeline stage: bounded by max_frames and ~512 MiB of device output per buffer
-  // (computed from whole-grid sizes, so every rank of a sharded plan takes the same stages)
+  // frames per pipeline stage: bounded by max_frames and ~512 MiB of device output per buffer,
+  // sized with quantities every rank of a sharded plan shares (whole grid when gathering, the
+  // largest shard otherwise) so all ranks take the same stages; the copies move the real rows
+  const int64_t rows_out = gather ? p->n_dirs_total : p->n_dirs;
+  const int64_t rows_size = gather ? p->n_dirs_total : sharded ? p->n_local_max : p->n_dirs;
   std::vector<size_t> out_frame_bytes;
   size_t out_frame_total = 0;
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((raw_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs_total * p->T * sizeof(float));
+    if ((raw_k >> k) & 1u) out_frame_bytes.push_back((size_t)rows_out * p->T * sizeof(float));
   for (int k = 0; k < dmas::N_KINDS; ++k)
-    if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)p->n_dirs_total * p->T_out * sizeof(float));
+    if ((env_k >> k) & 1u) out_frame_bytes.push_back((size_t)rows_out * p->T_out * sizeof(float));
   for (size_t b : out_frame_bytes) out_frame_total += b;
+  const size_t out_frame_size = out_frame_total / (size_t)rows_out * (size_t)rows_size;
+  const bool host_io = d2h;
   const size_t sig_frame = (size_t)p->n_mics * p->T_in * sizeof(float);
-  int32_t hc = (int32_t)std::max<size_t>(1, ((size_t)512 << 20) / out_frame_total);
+  int32_t hc = (int32_t)std::max<size_t>(1, ((size_t)512 << 20) / out_frame_size);
   hc = std::min({hc, p->max_frames, n_frames});
 
   for (auto& s : p->hs)
@@ -1066,7 +1076,7 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
     const int b = chunk_idx & 1;
     const int32_t nf = std::min(hc, n_frames - f0);
     if (chunk_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(p->hs[0], d2h_done[b], 0));
-    if (host_io)
+    if (h2d)
       CUDA_TRY(cudaMemcpyAsync(p->d_hsig[b], host_signals + (size_t)f0 * p->n_mics * p->T_in, sig_frame * nf,
                                cudaMemcpyHostToDevice, p->hs[0]));
     CUDA_TRY(cudaEventRecord(h2d_done[b], p->hs[0]));
@@ -1078,7 +1088,7 @@ dmas_status dmas_beamform_host(dmas_plan_t p, const float* host_signals, int32_t
       douts[i] = p->d_hout[b] + off / sizeof(float);
       off += out_frame_bytes[i] * nf;
     }
-    rc = beamform_device(p, p->d_hsig[b], nf, douts.data(), raw_k, env_k, DMAS_GATHER, p->hs[1]);
+    rc = beamform_device(p, p->d_hsig[b], nf, douts.data(), raw_k, env_k, gather ? DMAS_GATHER : 0u, p->hs[1]);
     if (rc != DMAS_OK) break;
     CUDA_TRY(cudaEventRecord(comp_done[b], p->hs[1]));
     CUDA_TRY(cudaStreamWaitEvent(p->hs[2], comp_done[b], 0));

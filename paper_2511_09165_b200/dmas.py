@@ -315,12 +315,25 @@ class Plan:
     def beamform_host(self, signals: Optional[np.ndarray], what: int, outs: Optional[list] = None,
                       n_frames: Optional[int] = None) -> Dict:
         """Host buffers in and out (synchronous).  Sharded plans: a collective; the root passes the
-        recording and receives the gathered images, the other ranks pass n_frames only."""
+        recording (the other ranks pass signals=None and n_frames); with GATHER in `what` the root
+        receives the whole images and the other ranks get {}, without it every rank receives its
+        own shard [F][n_local][.] in host memory."""
         if self.sharded and self.rank != self.root:
-            _check(lib.dmas_beamform_host(self._h, None, int(n_frames), None, what))
-            return {}
-        if self.sharded:
-            what |= GATHER
+            F = int(n_frames)
+            if what & GATHER:
+                _check(lib.dmas_beamform_host(self._h, None, F, None, what))
+                return {}
+            shapes = self.out_shapes(F, what)
+            if outs is None:
+                outs = [np.empty(s, dtype=np.float32) for (_, _, s) in shapes]
+            if len(outs) != len(shapes):
+                raise ValueError(f"{len(outs)} output buffers for {len(shapes)} requested outputs")
+            for o, (_, _, s) in zip(outs, shapes):
+                if o.shape != s or o.dtype != np.float32 or not o.flags.c_contiguous:
+                    raise ValueError(f"output buffer must be contiguous float32 {s}")
+            arr = (ctypes.c_void_p * max(1, len(outs)))(*[_host_ptr(o) for o in outs])
+            _check(lib.dmas_beamform_host(self._h, None, F, arr, what))
+            return {(stage, name): o for (stage, name, _), o in zip(shapes, outs)}
         if signals.dtype != np.float32 or not signals.flags.c_contiguous:
             raise TypeError("signals must be C-contiguous float32")
         if signals.ndim != 3 or signals.shape[1:] != (self.n_mics, self.n_samples + max(0, self.mf_taps - 1)):

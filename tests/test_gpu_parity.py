@@ -547,12 +547,14 @@ def test_sharded_plan_one_rank_bitwise(dm, what_name):
     assert np.array_equal(sp.delay_table(), plain.delay_table())
     resident = sp.beamform(x.clone(), what)
     gathered = sp.beamform(x.clone(), what | dm.GATHER)
-    host = sp.beamform_host(sig, what)
+    host = sp.beamform_host(sig, what)                      # every rank's shard into its host buffers
+    host_g = sp.beamform_host(sig, what | dm.GATHER)        # gathered onto the root, then to the host
     torch.cuda.synchronize()
     for k in ref:
         assert np.array_equal(resident[k].cpu().numpy(), ref[k]), ("resident", k)
         assert np.array_equal(gathered[k].cpu().numpy(), ref[k]), ("gathered", k)
         assert np.array_equal(host[k], ref[k]), ("host", k)
+        assert np.array_equal(host_g[k], ref[k]), ("host gathered", k)
     sp.close()
 
 

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps 2 --warmup 1 --force-sharded --no-cpu-baseline --no-extras --no-e2e --frames 32 > gpurun_out/bench_sharded3.json 2> gpurun_out/bench_sharded3.err; echo "rc=$?" >> gpurun_out/bench_sharded3.err
+B=paper_2511_09165_b200/build
+timeout 900 python tools/time_variants.py $B/libdmas_u4.so $B/libdmas_u8.so $B/libdmas_u32.so $B/libdmas_u4.so > gpurun_out/variants_u.log 2>&1
 echo done
