@@ -1,0 +1,114 @@
+"""Randomised GPU-vs-oracle parity over the plan space (seeded, reproducible).
+
+Each case draws an array (2..48 microphones in a disk or on a line), a direction grid (1..160
+directions in random order, some outside the array's main lobe), an order p (2..8, n_mics >= 2p for
+p >= 6), T (1..900 samples), 1..3 frames, a random subset of the image kinds at the raw and the
+envelope stage, and the plan options that select different kernels and paths: the classic or the
+LDS.64 beamformer, the tensor-core or FP32 envelope, nearest-sample or interpolated pre-steering, the
+matched filter, a band-pass, decimation, a tiny scratch budget (frame chunking) and cf_eps > 0
+(eps = 0 on all-zero pixels is 0/0; test_gpu_parity.py::test_cf_eps_zero_nonzero_input covers it).  Every
+requested output is compared with the float64 oracle under the north_star bar (1e-4 of the frame's
+peak; degenerate all-zero images against the input-amplitude bound, as in test_gpu_parity.py)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import dmas_oracle as O
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
+N_CASES = 240
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    p = int(rng.choice([2, 2, 2, 3, 3, 4, 5, 6, 7, 8]))
+    lo = 2 * p if p >= 6 else p
+    n_mics = int(rng.integers(lo, max(lo, 48) + 1))
+    if rng.random() < 0.25:
+        mic = gen.ula(n_mics, float(rng.uniform(2e-3, 5e-3)))
+    else:
+        mic = gen.disk_array(n_mics, float(rng.uniform(0.04, 0.12)), 2.5e-3, seed=int(rng.integers(1 << 30)))
+    n_dirs = int(rng.integers(1, 161))
+    dirs = np.stack([rng.uniform(-1.5, 1.5, n_dirs), rng.uniform(-1.0, 1.0, n_dirs)], axis=1)
+    T = int(rng.choice([1, 7, 33, 256, 300, 512, 640, 900]))
+    F = int(rng.integers(1, 4))
+    raw_k = [k for k in KINDS if rng.random() < 0.4]
+    env_k = [k for k in KINDS if rng.random() < 0.3]
+    if not raw_k and not env_k:
+        raw_k = ["cfdmas"]
+    opts = dict(bf_engine=int(rng.random() < 0.3), env_engine=int(rng.random() < 0.3),
+                delay_interp=int(rng.random() < 0.25), cf_eps=float(rng.choice([1e-30, 1e-6])))
+    if rng.random() < 0.2:
+        opts["scratch_bytes"] = 1                       # one frame per chunk
+    if env_k and rng.random() < 0.25:
+        L = int(rng.choice([31, 63, 127]))
+        opts.update(lp_taps=L, lp_cutoff_hz=float(rng.uniform(3e3, 2e4)))
+    if env_k and rng.random() < 0.2:
+        bp = (rng.standard_normal(int(rng.choice([3, 15]))) * 0.3).astype(np.float32)
+        opts["bp_coeffs"] = bp
+    if env_k and rng.random() < 0.2:
+        opts["env_decim"] = int(rng.integers(2, 5))
+    mf = None
+    if rng.random() < 0.2:
+        mf = rng.standard_normal(int(rng.integers(1, 40))).astype(np.float32)
+        opts["mf_coeffs"] = mf
+    Tin = T + (len(mf) - 1 if mf is not None else 0)
+    sig = gen.random_signals(F, n_mics, Tin, seed=int(rng.integers(1 << 30)), sparsity=float(rng.choice([0, 0.3])))
+    return dict(p=p, mic=mic, dirs=dirs, T=T, F=F, raw_k=raw_k, env_k=env_k, opts=opts, sig=sig, mf=mf)
+
+
+@pytest.fixture(scope="module")
+def dm():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2511_09165_b200 import dmas
+    return dmas
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_fuzz_parity(dm, seed):
+    import torch
+    c = _case(seed)
+    what = 0
+    for k in c["raw_k"]:
+        what |= dm.RAW(dm.KIND_BITS[k])
+    for k in c["env_k"]:
+        what |= dm.ENV(dm.KIND_BITS[k])
+    plan = dm.Plan(c["mic"], c["dirs"], gen.FS, gen.C_SOUND, c["p"], c["T"], max_frames=c["F"], **c["opts"])
+    res = plan.beamform(torch.from_numpy(c["sig"]).cuda(), what)
+    torch.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in res.items()}
+    # oracle
+    o = c["opts"]
+    m = O.matched_filter(c["sig"], c["mf"], c["T"]) if c["mf"] is not None else c["sig"].astype(np.float64)
+    if o["delay_interp"]:
+        d, al = O.delay_table(c["mic"], c["dirs"], gen.FS, gen.C_SOUND, mode="linear")
+        assert np.array_equal(plan.delay_table(), d)
+    else:
+        d, al = O.delay_table(c["mic"], c["dirs"], gen.FS, gen.C_SOUND), None
+        assert np.array_equal(plan.delay_table(), d)
+    h = O.lpf_taps(o.get("lp_taps", 127), o.get("lp_cutoff_hz", 5000.0), gen.FS)
+    bp = o.get("bp_coeffs")
+    scale = (math.comb(len(c["mic"]), c["p"]) + len(c["mic"])) * max(float(np.max(np.abs(m))), 1e-30)
+    for f in range(c["F"]):
+        img = O.beamform_frame(m[f], d, c["p"], eps=o["cf_eps"], alpha=al)
+        for stage, kinds in (("raw", c["raw_k"]), ("env", c["env_k"])):
+            for k in kinds:
+                ref = img[k] if stage == "raw" else O.envelope(img[k], h, bp_taps=None if bp is None else
+                                                               bp.astype(np.float64), decim=o.get("env_decim", 1))
+                g = got[(stage, k)][f]
+                assert g.shape == ref.shape, (seed, stage, k)
+                assert np.all(np.isfinite(g)), (seed, stage, k)
+                peak = float(np.max(np.abs(ref)))
+                err = float(np.max(np.abs(g.astype(np.float64) - ref))) if ref.size else 0.0
+                bound = TOL * peak if peak > 0 else TOL * scale
+                assert err <= bound, (f"seed {seed} p={c['p']} n_mics={len(c['mic'])} n_dirs={len(c['dirs'])} "
+                                      f"T={c['T']} {stage}/{k} opts={ {k2: v for k2, v in o.items() if k2 != 'bp_coeffs' and k2 != 'mf_coeffs'} }: "
+                                      f"err {err:.3e} > {bound:.3e} (peak {peak:.3e})")
+    plan.close()

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-B=paper_2511_09165_b200/build
-timeout 900 python tools/time_variants.py $B/libdmas_u4.so $B/libdmas_u8.so $B/libdmas_u32.so $B/libdmas_u4.so > gpurun_out/variants_u.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_fuzz.py -m gpu -q -rf > gpurun_out/pytest_fuzz.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_fuzz.log
 echo done
