@@ -557,7 +557,7 @@ def run_ours(args, rank, world, local):
         e2e = {"value": e_px / et, "unit": UNIT,
                "h2d_bytes_per_step": int(Fe * n_mics * T * 4) * (world if args.mode == "weak" else 1),
                "d2h_bytes_per_step": int(e_px * 4), "frames_per_step": Fe,
-               "ratio_to_device_value": (e_px / et) / value,
+               "ratio_to_device_value": (e_px / et) / value, "seconds_per_step": et,
                "timing": "host wall clock around the synchronous dmas_beamform_host call, max over ranks (pinned "
                          "host buffers; H2D, kernels and D2H pipelined in chunks; sharded: the root's recording in, "
                          "broadcast on the device, every rank's image shard out over its own PCIe link); bound by "
@@ -585,6 +585,9 @@ def run_ours(args, rank, world, local):
         if gathered:
             line["gathered"] = gathered
         line.update(extras)
+        if e2e and extras.get("pcie_d2h_GB_s"):
+            e2e["d2h_GB_s"] = e2e["d2h_bytes_per_step"] / e2e["seconds_per_step"] / 1e9
+            e2e["frac_of_measured_pcie_d2h"] = e2e["d2h_GB_s"] / extras["pcie_d2h_GB_s"]
         emit(line)
     if sharded:
         sb.close()
@@ -664,6 +667,12 @@ def gpu_extras(args, cfg, plan, x, out, kw, dmas, torch, dev, stream, value):
                          "note": "C1: 8-mic ULA, 91 directions, T = 1024, CF-DMAS2 envelope; one dmas_beamform call "
                                  "per frame (roots, beamform, envelope); graph = 100 calls captured once, replayed"}
     pc.close()
+
+    # the e2e's bound: device-to-host copy bandwidth into pinned memory (PCIe), 2 GiB copies
+    src = flat[: (2 << 30) // 4]
+    dst = torch.empty(src.numel(), dtype=torch.float32, pin_memory=True)
+    d2h = time_fn(lambda: dst.copy_(src, non_blocking=True), 3)
+    res["pcie_d2h_GB_s"] = src.numel() * 4 / (d2h * 1e-3) / 1e9
     return res
 
 

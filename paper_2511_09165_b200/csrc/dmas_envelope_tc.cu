@@ -81,7 +81,14 @@ constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (T
 #endif
 constexpr int NCP = DMAS_TC_NCP;
 static_assert(NCP >= 0 && NCP <= 5, "NCP");
-constexpr int NCOPYW = NCP < 5 ? 4 : 0;            // copy warps (one TMEM lane quarter each)
+#ifndef DMAS_TC_COPYW
+#define DMAS_TC_COPYW 4
+#endif
+#ifndef DMAS_TC_CONVW
+#define DMAS_TC_CONVW 8
+#endif
+constexpr int NCOPYW = NCP < 5 ? DMAS_TC_COPYW : 0;  // copy warps: 4 (one per TMEM lane quarter) or 8
+                                                    // (two per quarter, alternate shifts)
 // epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, 16 output columns each)
 #ifndef DMAS_TC_EPIW
 #define DMAS_TC_EPIW 4
@@ -93,7 +100,7 @@ constexpr int EPI_COLS = BLK * 4 / EPIW;            // output columns per epilog
 constexpr int EPI_WARP0 = 0;                        // TMEM accumulator -> clamp -> TMA store
 constexpr int COPY_WARP0 = EPIW;                    // the other shifted A copies (LDS + tcgen05.st)
 constexpr int CONV_WARP0 = COPY_WARP0 + NCOPYW;     // 8 warps: fp32 stage -> bf16 hi / lo buffer
-constexpr int CONV_WARPS = 8;
+constexpr int CONV_WARPS = DMAS_TC_CONVW;
 constexpr int MMA_WARP = CONV_WARP0 + CONV_WARPS;
 constexpr int TMA_WARP = MMA_WARP + 1;
 constexpr int CONV_THREADS = CONV_WARPS * 32;
@@ -418,9 +425,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     }
   } else if (warp >= COPY_WARP0 && warp < COPY_WARP0 + NCOPYW) {
     // ================= copy warps: shifts NCP..4 of TMEM lane tau (hi and lo), LDS.128 + tcgen05.st
-    const int quarter = warp - COPY_WARP0;
+    const int quarter = (warp - COPY_WARP0) & 3, part = (warp - COPY_WARP0) >> 2;
     const int tau = 32 * quarter + lane;
     const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    constexpr int QSTEP = NCOPYW / 4;
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int buf = (int)(jj & 1);
       PROF_WAIT(0, mbar_wait(&conv_full[buf], (uint32_t)((jj >> 1) & 1)));
@@ -429,7 +437,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
       const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS);
 #pragma unroll
-      for (int qi = NCP; qi < NQ; ++qi) {
+      for (int qi = NCP + part; qi < NQ; qi += QSTEP) {
         const uint32_t row = cv + (uint32_t)((tau + qi) * 16);          // block row tau + q
         uint4 hv[4], lv[4];
 #pragma unroll
