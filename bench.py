@@ -53,7 +53,7 @@ FP32_LANES_PER_SM_CLK = 128     # FFMA/FADD/FMUL lanes per SM per clock (guide; 
 # beamform = N_m * phi_p + 30, phi_p = 5 / 6 / 9 / 10 for p = 2 / 3 / 4 / 5
 PHI_P = {2: 5, 3: 6, 4: 9, 5: 10}
 # FP32-pipe lane-ops per microphone sample of k_beamform_lds64 as issued and per pixel epilogue
-OPS_PER_MIC = {2: 5, 3: 6, 4: 10, 5: 10}
+OPS_PER_MIC = {2: 5, 3: 6, 4: 9, 5: 9}
 OPS_EPI = {2: 6, 3: 10, 4: 14, 5: 18}
 BF_KERNELS = {0: "k_beamform", 1: "k_beamform_lds64", 2: "k_beamform_mg"}   # dmas_plan_info.bf_kernel
 SURVEY_F2_CEILING = {"C5": 131e9 / 1e9, "C4": 73e9 / 1e9}    # SURVEY.md §8(d) model ceilings, Gpx/s per GPU

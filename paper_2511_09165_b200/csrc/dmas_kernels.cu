@@ -283,12 +283,14 @@ template <> __device__ __forceinline__ void acc_add<4>(Acc<4>& c, float s) {
   c.b = fmaf(s4, s4, c.b);
 }
 template <> __device__ __forceinline__ void acc_add<5>(Acc<5>& c, float s) {
+  // 9 FP32 operations: s^4 is never formed on its own -- P4 takes s2*s2 as an FFMA and x = s^5 is
+  // s3 * s2
   const float s2 = __fmul_rn(s, s);
   const float s3 = __fmul_rn(s2, s);
-  const float s4 = __fmul_rn(s2, s2);
-  const float x = __fmul_rn(s4, s);
+  const float x = __fmul_rn(s3, s2);
   c.p12 = __fadd2_rn(c.p12, make_float2(s, s2));
-  c.p34 = __fadd2_rn(c.p34, make_float2(s3, s4));
+  c.p34.x = __fadd_rn(c.p34.x, s3);
+  c.p34.y = fmaf(s2, s2, c.p34.y);
   c.a = __fadd_rn(c.a, x);
   c.b = fmaf(x, x, c.b);
 }
@@ -830,15 +832,14 @@ template <> struct PAcc<4> {
 template <> struct PAcc<5> {
   float2 p1, p2, p3, p4, a, b;
   __device__ __forceinline__ void zero() { p1 = p2 = p3 = p4 = a = b = f2(0.f, 0.f); }
-  __device__ __forceinline__ void add2(const float2& s) {
+  __device__ __forceinline__ void add2(const float2& s) {   // = acc_add<5> per lane
     const float2 s2 = mul2s(s, s);
     const float2 s3 = mul2s(s2, s);
-    const float2 s4 = mul2s(s2, s2);
-    const float2 x = mul2s(s4, s);
+    const float2 x = mul2s(s3, s2);
     p1 = __fadd2_rn(p1, s);
     p2 = __fadd2_rn(p2, s2);
     p3 = __fadd2_rn(p3, s3);
-    p4 = __fadd2_rn(p4, s4);
+    p4 = __ffma2_rn(s2, s2, p4);
     a = __fadd2_rn(a, x);                             // = P5
     b = __ffma2_rn(x, x, b);
   }

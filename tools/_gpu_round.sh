@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-B=paper_2511_09165_b200/build
-timeout 900 python tools/time_variants.py $B/libdmas_k4c8.so $B/libdmas_k8c8.so $B/libdmas_k8c6.so $B/libdmas_k4c6.so $B/libdmas_k4c10.so $B/libdmas_k8c6p.so $B/libdmas_k4c8.so > gpurun_out/variants_k.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -m gpu -x -q -k "C3 or slice or lds64 or fuzz or random_multi or high_orders" > gpurun_out/pytest_p5.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_p5.log
 echo done
