@@ -210,6 +210,24 @@ def test_config_C4_whole_frame_all_kinds(dm):
     _assert_whole_frames(compare_frames(sig, d, 3, gpu, [0], chunk=128), "C4")
 
 
+def test_config_C5_frame_all_kinds_whole_frame(dm):
+    """C5 frame 200 (3 reflectors advanced 0.2 m, its own noise), every kind raw and envelope, over
+    the whole 67 M-pixel frame against the oracle."""
+    import torch
+    from _oracle_pool import compare_frames
+    cfg = gen.config("C5", frames=201)
+    sig = np.ascontiguousarray(cfg["signals"][200:201])
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=1)
+    res = plan.beamform(torch.from_numpy(sig).cuda(), what_all(dm))
+    torch.cuda.synchronize()
+    gpu = {k: v.cpu().numpy() for k, v in res.items()}
+    del res
+    d = plan.delay_table()
+    r = compare_frames(sig, d, 2, gpu, [0])
+    assert len(r) == 10
+    _assert_whole_frames(r, "C5 f200")
+
+
 def test_config_C5_bench_launch_whole_frames(dm):
     """C5 in the launch configuration bench.py times: one call over 256 frames, CF-DMAS2 envelope
     only (the raw image goes through the plan scratch in internal frame chunks).  Frames
