@@ -1,6 +1,7 @@
 """Randomised GPU-vs-oracle parity over the plan space (seeded, reproducible).
 
-Each case draws an array (2..48 microphones in a disk or on a line), a direction grid (1..160
+Each case draws an array (2..48 microphones in a disk or on a line; 24 more cases with 80..320
+microphones in a 20 cm disk, which take the microphone-group kernel), a direction grid (1..160
 directions in random order, some outside the array's main lobe), an order p (2..8, n_mics >= 2p for
 p >= 6), T (1..900 samples), 1..3 frames, a random subset of the image kinds at the raw and the
 envelope stage, and the plan options that select different kernels and paths: the classic or the
@@ -23,20 +24,23 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
 N_CASES = 240
+N_LARGE = 24              # cases with 80..320 microphones (the microphone-group kernel)
 
 
-def _case(seed):
-    rng = np.random.default_rng(1000 + seed)
+def _case(seed, large=False):
+    rng = np.random.default_rng(1000 + seed + (100000 if large else 0))
     p = int(rng.choice([2, 2, 2, 3, 3, 4, 5, 6, 7, 8]))
     lo = 2 * p if p >= 6 else p
-    n_mics = int(rng.integers(lo, max(lo, 48) + 1))
-    if rng.random() < 0.25:
+    n_mics = int(rng.integers(lo, max(lo, 48) + 1)) if not large else int(rng.integers(80, 321))
+    if large:                                   # arrays too big for one staged window: the
+        mic = gen.disk_array(n_mics, 0.2, 2.5e-3, seed=int(rng.integers(1 << 30)))   # microphone-group path
+    elif rng.random() < 0.25:
         mic = gen.ula(n_mics, float(rng.uniform(2e-3, 5e-3)))
     else:
         mic = gen.disk_array(n_mics, float(rng.uniform(0.04, 0.12)), 2.5e-3, seed=int(rng.integers(1 << 30)))
-    n_dirs = int(rng.integers(1, 161))
+    n_dirs = int(rng.integers(1, 161 if not large else 41))
     dirs = np.stack([rng.uniform(-1.5, 1.5, n_dirs), rng.uniform(-1.0, 1.0, n_dirs)], axis=1)
-    T = int(rng.choice([1, 7, 33, 256, 300, 512, 640, 900]))
+    T = int(rng.choice([1, 7, 33, 256, 300, 512, 640, 900] if not large else [33, 300, 512]))
     F = int(rng.integers(1, 4))
     raw_k = [k for k in KINDS if rng.random() < 0.4]
     env_k = [k for k in KINDS if rng.random() < 0.3]
@@ -73,8 +77,17 @@ def dm():
 
 @pytest.mark.parametrize("seed", range(N_CASES))
 def test_fuzz_parity(dm, seed):
+    _run_case(dm, seed, False)
+
+
+@pytest.mark.parametrize("seed", range(N_LARGE))
+def test_fuzz_parity_large_arrays(dm, seed):
+    _run_case(dm, seed, True)
+
+
+def _run_case(dm, seed, large):
     import torch
-    c = _case(seed)
+    c = _case(seed, large)
     what = 0
     for k in c["raw_k"]:
         what |= dm.RAW(dm.KIND_BITS[k])
