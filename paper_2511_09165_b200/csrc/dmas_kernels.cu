@@ -909,16 +909,6 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
   mbar_wait(&bar, 0);
 
   const uint32_t la = smem_u32(win) + 8u * (uint32_t)lane;
-  // k-d tiles: the image rows of this warp's directions (q = warp + 8 i), fetched once per CTA --
-  // lane i holds the i-th -- and broadcast with a shuffle per direction (a dependent global load per
-  // direction stalled the warp before its epilogue)
-  int32_t psi_lane = 0;
-  if (a.psi_map && lane < QP / BF_WARPS && warp + BF_WARPS * lane < npsi)
-    psi_lane = __ldg(a.psi_map + psi0 + warp + BF_WARPS * lane);
-  auto row_of = [&](int q) -> int64_t {
-    const int32_t r = __shfl_sync(0xffffffffu, psi_lane, (q - warp) / BF_WARPS);
-    return a.psi_map ? (int64_t)r : psi0 + q;
-  };
   if constexpr (KM == 1 && !INTERP) {
     // DAS-only request (Eq. (2)): the prologue wrote the identity plane (x = m, no
     // roots), so the sum over microphones is one packed FADD2 per pixel pair and LDS.64
@@ -939,7 +929,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
             for (int m = 0; m < KT / 2; ++m) acc[m] = __fadd2_rn(acc[m], lds_f32x2(la + (uint32_t)oo[h] + 512u * m));
         }
       }
-      const int64_t psi = row_of(q);
+      const int64_t psi = a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q;
       const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
 #pragma unroll
       for (int k = 0; k < KT; ++k)
@@ -990,7 +980,7 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
     Acc<P> px[KT];                                  // pixel t0 + lane + 32 k
 #pragma unroll
     for (int k = 0; k < KT; ++k) px[k] = acc[k >> 1].get(k & 1);   // LDS m holds pixels 2m, 2m + 1
-    bf_epilogue<P, KM, KT>(a, px, f, row_of(q), t0, lane);
+    bf_epilogue<P, KM, KT>(a, px, f, a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q, t0, lane);
   }
 }
 

@@ -22,7 +22,9 @@ from paper_2511_09165_b200 import dmas
 F = 16
 cfg = gen.config("C5", frames=F)
 x = torch.from_numpy(cfg["signals"]).cuda()
-plan = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=F)
+import os
+KW = json.loads(os.environ.get("DMAS_TV_KW", "{}"))      # extra plan options, e.g. {"delay_interp": 1}
+plan = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=F, **KW)
 out = torch.empty((F, len(cfg["dirs"]), cfg["T"]), dtype=torch.float32, device="cuda")
 what = dmas.ENV(dmas.KIND_CFDMAS)
 for _ in range(3):
@@ -37,8 +39,11 @@ h = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]
 rec = {"lib": LIB, "env_ms": t["envelope"][0] / t["envelope"][1], "bf_ms": t["beamform"][0] / t["beamform"][1], "sha": h}
 from oracle import dmas_oracle as O                 # sanity: 128 rows of frame 0 against the oracle
 rows = np.linspace(0, len(cfg["dirs"]) - 1, 128).astype(int)
-d = O.delay_table(cfg["mic_xyz"], cfg["dirs"][rows], cfg["fs"], cfg["c"])
-ref = O.envelope(O.beamform_frame(cfg["signals"][0], d, 2)["cfdmas"], O.lpf_taps())
+if KW.get("delay_interp"):
+    d, al = O.delay_table(cfg["mic_xyz"], cfg["dirs"][rows], cfg["fs"], cfg["c"], mode="linear")
+else:
+    d, al = O.delay_table(cfg["mic_xyz"], cfg["dirs"][rows], cfg["fs"], cfg["c"]), None
+ref = O.envelope(O.beamform_frame(cfg["signals"][0], d, 2, alpha=al)["cfdmas"], O.lpf_taps())
 got = out[0].cpu().numpy()[rows]
 rec["oracle_rel_err"] = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
 try:                                     # role-wait profile (builds with -DDMAS_TC_PROFILE)
