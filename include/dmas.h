@@ -136,7 +136,12 @@ typedef struct {
   int32_t rank;              /* this process's rank in [0, n_ranks)                              */
   int32_t root;              /* rank holding the signals and receiving gathered images           */
   const uint8_t* comm_id;    /* DMAS_COMM_ID_BYTES from dmas_comm_id() on one rank, shared with
-                                every rank out of band (e.g. a torch.distributed broadcast)      */
+                                every rank out of band (e.g. a torch.distributed broadcast).
+                                An id whose first 8 bytes are "DMASLOOP" selects the in-process
+                                loopback transport instead of NCCL (test infrastructure: all
+                                ranks are plans of one process, driven from concurrent threads;
+                                the exchange runs as event-ordered device copies with NCCL's
+                                matching and completion semantics)                               */
 } dmas_plan_desc;
 
 /* Fill `desc` with defaults (zero geometry; order 2; cf_eps 1e-30; lp 127 taps at 5 kHz;

@@ -6,8 +6,12 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <tuple>
 
 #include <nccl.h>
 
@@ -133,10 +137,85 @@ dmas_status nccl_fail(ncclResult_t r, const char* what, std::string& err) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------- loopback
+// In-process test transport (comm_id starting with "DMASLOOP"): the ranks are plans of ONE
+// process -- threads, on any devices -- and the exchange runs as device-to-device copies ordered
+// by CUDA events, with NCCL's semantics: operations match in issue order per peer pair, a
+// broadcast / send completes on the sender's stream only once the receivers' copies are done
+// (so the sender may then reuse its buffer).  Every rank thread blocks (host side) until its
+// peers have enqueued their side of an operation, as NCCL's ranks progress together.  It lets
+// the multi-rank exchange of the runtime (chunk agreement, staging reuse, gather assembly, host
+// path) run on one GPU without two ranks ever waiting on each other inside a kernel.
+namespace {
+struct LoopMsg {
+  const void* src = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ready = nullptr;            // recorded on the sender's stream after its data is ready
+  std::vector<cudaEvent_t> done;          // recorded on each receiver's stream after its copy
+};
+struct LoopGroup {
+  std::mutex mu;
+  std::condition_variable cv;
+  int32_t n_ranks = 0;
+  int ar_count = 0;
+  int64_t ar_gen = 0, ar_acc = 0, ar_result = 0;
+  std::map<int64_t, LoopMsg> bcast;                                   // by broadcast sequence
+  std::map<std::tuple<int32_t, int32_t, int64_t>, LoopMsg> p2p;       // (src, dst, sequence)
+};
+std::mutex g_loop_mu;
+std::map<std::string, std::weak_ptr<LoopGroup>> g_loop_groups;
+constexpr char kLoopMagic[8] = {'D', 'M', 'A', 'S', 'L', 'O', 'O', 'P'};
+}  // namespace
+
 struct Comm {
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;        // loopback transport (tests), else NCCL
   int32_t n_ranks = 1, rank = 0;
+  int64_t bseq = 0;                       // loopback: broadcasts issued
+  std::map<int32_t, int64_t> sseq, rseq;  // loopback: sends to / receives from each peer
 };
+
+namespace {
+dmas_status cuda_fail(cudaError_t e, const char* what, std::string& err) {
+  err = std::string(what) + ": " + cudaGetErrorString(e);
+  return DMAS_ERR_CUDA;
+}
+#define LOOP_TRY(expr, what)                                    \
+  do {                                                          \
+    cudaError_t e_ = (expr);                                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what, err);     \
+  } while (0)
+
+// sender side: publish `src` (ready once `st` reaches this point), then make `st` wait until
+// every one of `n_recv` receivers has copied it
+dmas_status loop_publish_and_wait(LoopGroup& g, LoopMsg* slot_owner_check, std::unique_lock<std::mutex>& lk,
+                                  LoopMsg& m, size_t n_recv, cudaStream_t st, std::string& err) {
+  (void)slot_owner_check;
+  g.cv.notify_all();
+  g.cv.wait(lk, [&] { return m.done.size() >= n_recv; });
+  for (cudaEvent_t e : m.done) {
+    LOOP_TRY(cudaStreamWaitEvent(st, e, 0), "loopback: wait for receivers");
+    cudaEventDestroy(e);
+  }
+  cudaEventDestroy(m.ready);
+  return DMAS_OK;
+}
+// receiver side: copy the published message into `dst` on `st`, then report done
+dmas_status loop_receive(LoopGroup& g, LoopMsg& m, void* dst, size_t bytes, cudaStream_t st, std::string& err) {
+  if (m.bytes != bytes) {
+    err = "loopback: message size mismatch (" + std::to_string(m.bytes) + " vs " + std::to_string(bytes) + ")";
+    return DMAS_ERR_NCCL;
+  }
+  LOOP_TRY(cudaStreamWaitEvent(st, m.ready, 0), "loopback: wait for sender");
+  if (dst != m.src) LOOP_TRY(cudaMemcpyAsync(dst, m.src, bytes, cudaMemcpyDefault, st), "loopback: copy");
+  cudaEvent_t d = nullptr;
+  LOOP_TRY(cudaEventCreateWithFlags(&d, cudaEventDisableTiming), "loopback: event");
+  LOOP_TRY(cudaEventRecord(d, st), "loopback: record");
+  m.done.push_back(d);
+  g.cv.notify_all();
+  return DMAS_OK;
+}
+}  // namespace
 
 dmas_status unique_id(uint8_t out[DMAS_COMM_ID_BYTES], std::string& err) {
   static_assert(DMAS_COMM_ID_BYTES == NCCL_UNIQUE_ID_BYTES, "comm id size");
@@ -153,6 +232,26 @@ dmas_status unique_id(uint8_t out[DMAS_COMM_ID_BYTES], std::string& err) {
 
 dmas_status create(const uint8_t id[DMAS_COMM_ID_BYTES], int32_t n_ranks, int32_t rank, Comm** out,
                    std::string& err) {
+  if (std::memcmp(id, kLoopMagic, sizeof(kLoopMagic)) == 0) {
+    const std::string key(reinterpret_cast<const char*>(id), DMAS_COMM_ID_BYTES);
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    std::shared_ptr<LoopGroup> g = g_loop_groups[key].lock();
+    if (!g) {
+      g = std::make_shared<LoopGroup>();
+      g->n_ranks = n_ranks;
+      g_loop_groups[key] = g;
+    }
+    if (g->n_ranks != n_ranks) {
+      err = "loopback: ranks disagree on n_ranks";
+      return DMAS_ERR_NCCL;
+    }
+    auto* c = new Comm();
+    c->loop = g;
+    c->n_ranks = n_ranks;
+    c->rank = rank;
+    *out = c;
+    return DMAS_OK;
+  }
   const Api& a = api();
   if (!a.loaded) {
     err = a.why;
@@ -174,6 +273,10 @@ dmas_status create(const uint8_t id[DMAS_COMM_ID_BYTES], int32_t n_ranks, int32_
 
 void destroy(Comm* c) {
   if (!c) return;
+  if (c->loop) {
+    delete c;
+    return;
+  }
   const Api& a = api();
   if (c->comm && a.loaded) {
     ncclResult_t ae = ncclSuccess;
@@ -185,11 +288,45 @@ void destroy(Comm* c) {
 }
 
 dmas_status broadcast(Comm* c, float* buf, size_t count, int32_t root, cudaStream_t st, std::string& err) {
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    const int64_t seq = c->bseq++;
+    const size_t bytes = count * sizeof(float);
+    std::unique_lock<std::mutex> lk(g.mu);
+    if (c->rank == root) {
+      LoopMsg& m = g.bcast[seq];
+      m.src = buf;
+      m.bytes = bytes;
+      LOOP_TRY(cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming), "loopback: event");
+      LOOP_TRY(cudaEventRecord(m.ready, st), "loopback: record");
+      dmas_status rc = loop_publish_and_wait(g, nullptr, lk, m, (size_t)(c->n_ranks - 1), st, err);
+      g.bcast.erase(seq);
+      return rc;
+    }
+    g.cv.wait(lk, [&] { auto it = g.bcast.find(seq); return it != g.bcast.end() && it->second.ready; });
+    return loop_receive(g, g.bcast[seq], buf, bytes, st, err);
+  }
   NCCL_TRY(api().Broadcast(buf, buf, count, ncclFloat32, root, c->comm, st), "ncclBroadcast");
   return DMAS_OK;
 }
 
 dmas_status allreduce_min(Comm* c, int64_t* v, cudaStream_t st, std::string& err) {
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    std::unique_lock<std::mutex> lk(g.mu);
+    const int64_t gen = g.ar_gen;
+    g.ar_acc = g.ar_count == 0 ? *v : std::min(g.ar_acc, *v);
+    if (++g.ar_count == g.n_ranks) {
+      g.ar_result = g.ar_acc;
+      g.ar_count = 0;
+      ++g.ar_gen;
+      g.cv.notify_all();
+    } else {
+      g.cv.wait(lk, [&] { return g.ar_gen != gen; });
+    }
+    *v = g.ar_result;
+    return DMAS_OK;
+  }
   int64_t* d = nullptr;
   if (cudaMalloc(&d, sizeof(int64_t)) != cudaSuccess) {
     err = "cudaMalloc (allreduce scratch)";
@@ -226,6 +363,30 @@ dmas_status run_gather(Comm* c, const std::vector<dmas_xfer>& xs, const float* s
   bool any = false;
   for (const dmas_xfer& x : xs) any |= x.kind != DMAS_XFER_COPY;
   if (!any) return DMAS_OK;
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    for (const dmas_xfer& x : xs) {
+      const size_t bytes = (size_t)x.count * sizeof(float);
+      std::unique_lock<std::mutex> lk(g.mu);
+      if (x.kind == DMAS_XFER_SEND) {
+        const auto key = std::make_tuple(c->rank, x.peer, c->sseq[x.peer]++);
+        LoopMsg& m = g.p2p[key];
+        m.src = shard + x.src_elem;
+        m.bytes = bytes;
+        LOOP_TRY(cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming), "loopback: event");
+        LOOP_TRY(cudaEventRecord(m.ready, st), "loopback: record");
+        dmas_status rc = loop_publish_and_wait(g, nullptr, lk, m, 1, st, err);
+        g.p2p.erase(key);
+        if (rc != DMAS_OK) return rc;
+      } else if (x.kind == DMAS_XFER_RECV) {
+        const auto key = std::make_tuple(x.peer, c->rank, c->rseq[x.peer]++);
+        g.cv.wait(lk, [&] { auto it = g.p2p.find(key); return it != g.p2p.end() && it->second.ready; });
+        dmas_status rc = loop_receive(g, g.p2p[key], dst + x.dst_elem, bytes, st, err);
+        if (rc != DMAS_OK) return rc;
+      }
+    }
+    return DMAS_OK;
+  }
   NCCL_TRY(a.GroupStart(), "ncclGroupStart");
   for (const dmas_xfer& x : xs) {
     ncclResult_t r = ncclSuccess;

@@ -164,6 +164,12 @@ def comm_id() -> bytes:
     return bytes(buf)
 
 
+def loopback_comm_id() -> bytes:
+    """A comm id for the library's in-process loopback transport (include/dmas.h comm_id): the
+    ranks of a sharded plan as plans of this process driven from concurrent threads (tests)."""
+    return b"DMASLOOP" + os.urandom(COMM_ID_BYTES - 8)
+
+
 def shard_range(n_dirs: int, n_ranks: int, rank: int):
     """dmas_shard_range: the contiguous grid rows [g0, g1) `rank` owns."""
     g0, g1 = ctypes.c_int64(), ctypes.c_int64()
