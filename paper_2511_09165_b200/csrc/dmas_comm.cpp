@@ -188,9 +188,8 @@ dmas_status cuda_fail(cudaError_t e, const char* what, std::string& err) {
 
 // sender side: publish `src` (ready once `st` reaches this point), then make `st` wait until
 // every one of `n_recv` receivers has copied it
-dmas_status loop_publish_and_wait(LoopGroup& g, LoopMsg* slot_owner_check, std::unique_lock<std::mutex>& lk,
-                                  LoopMsg& m, size_t n_recv, cudaStream_t st, std::string& err) {
-  (void)slot_owner_check;
+dmas_status loop_publish_and_wait(LoopGroup& g, std::unique_lock<std::mutex>& lk, LoopMsg& m, size_t n_recv,
+                                  cudaStream_t st, std::string& err) {
   g.cv.notify_all();
   g.cv.wait(lk, [&] { return m.done.size() >= n_recv; });
   for (cudaEvent_t e : m.done) {
@@ -299,7 +298,7 @@ dmas_status broadcast(Comm* c, float* buf, size_t count, int32_t root, cudaStrea
       m.bytes = bytes;
       LOOP_TRY(cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming), "loopback: event");
       LOOP_TRY(cudaEventRecord(m.ready, st), "loopback: record");
-      dmas_status rc = loop_publish_and_wait(g, nullptr, lk, m, (size_t)(c->n_ranks - 1), st, err);
+      dmas_status rc = loop_publish_and_wait(g, lk, m, (size_t)(c->n_ranks - 1), st, err);
       g.bcast.erase(seq);
       return rc;
     }
@@ -375,7 +374,7 @@ dmas_status run_gather(Comm* c, const std::vector<dmas_xfer>& xs, const float* s
         m.bytes = bytes;
         LOOP_TRY(cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming), "loopback: event");
         LOOP_TRY(cudaEventRecord(m.ready, st), "loopback: record");
-        dmas_status rc = loop_publish_and_wait(g, nullptr, lk, m, 1, st, err);
+        dmas_status rc = loop_publish_and_wait(g, lk, m, 1, st, err);
         g.p2p.erase(key);
         if (rc != DMAS_OK) return rc;
       } else if (x.kind == DMAS_XFER_RECV) {
