@@ -372,6 +372,68 @@ def test_chunking_and_sharding_bitwise(dm):
                 assert np.array_equal(a[k][:, g0:g1], r[k].cpu().numpy()), (G, k)
 
 
+def test_calls_on_different_streams_are_ordered(dm):
+    """Two calls on one plan issued back to back on two unrelated streams (both use the plan's
+    signed-root plane and scratch): the second waits for the first through the plan-owned event,
+    so both results equal the sequential ones (cross-stream race)."""
+    import torch
+    cfg = gen.config("C3")
+    sig_a = cfg["signals"]
+    sig_b = gen.random_signals(1, 32, cfg["T"], seed=58)
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 3, cfg["T"])
+    what = dm.ENV(dm.KIND_CFDMAS) | dm.RAW(dm.KIND_DAS)
+    xa, xb = torch.from_numpy(sig_a).cuda(), torch.from_numpy(sig_b).cuda()
+    ref_a = {k: v.cpu().numpy() for k, v in plan.beamform(xa, what).items()}
+    ref_b = {k: v.cpu().numpy() for k, v in plan.beamform(xb, what).items()}
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs_a = [torch.empty(s, device="cuda") for (_, _, s) in plan.out_shapes(1, what)]
+    outs_b = [torch.empty(s, device="cuda") for (_, _, s) in plan.out_shapes(1, what)]
+    for _ in range(3):
+        plan.beamform(xa, what, outs=outs_a, stream=s1)
+        plan.beamform(xb, what, outs=outs_b, stream=s2)
+    torch.cuda.synchronize()
+    for i, (stage, kind, _) in enumerate(plan.out_shapes(1, what)):
+        assert np.array_equal(outs_a[i].cpu().numpy(), ref_a[(stage, kind)]), (stage, kind)
+        assert np.array_equal(outs_b[i].cpu().numpy(), ref_b[(stage, kind)]), (stage, kind)
+
+
+def test_calls_do_not_allocate_and_graph_replay(dm):
+    """dmas_beamform allocates nothing (device free memory unchanged across calls, envelope scratch
+    included), so a sequence of calls can be captured in a CUDA graph; the replayed images equal
+    the eager ones."""
+    import torch
+    cfg = gen.config("C1")
+    plan = dm.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 2, cfg["T"], max_frames=1)
+    what = dm.ENV(dm.KIND_CFDMAS | dm.KIND_DAS)
+    x = torch.from_numpy(cfg["signals"]).cuda()
+    outs = [torch.empty(s, device="cuda") for (_, _, s) in plan.out_shapes(1, what)]
+    plan.beamform(x, what, outs=outs)
+    torch.cuda.synchronize()
+    eager = [o.cpu().numpy() for o in outs]
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        plan.beamform(x, what, outs=outs)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] == free0
+    for o in outs:
+        o.zero_()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(4):
+                plan.beamform(x, what, outs=outs)
+    torch.cuda.synchronize()
+    for o in outs:
+        o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for o, e in zip(outs, eager):
+        assert np.array_equal(o.cpu().numpy(), e)
+
+
 def test_timing_and_launch_counter(dm):
     import torch
     plan = dm.Plan(gen.ula(8), gen.az_grid_deg(np.arange(-90, 91, 2)), gen.FS, gen.C_SOUND, 2, 1024, max_frames=4)
