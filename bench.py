@@ -86,6 +86,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip all_fp32 / linearity / C1 latency")
     ap.add_argument("--cpu-dirs", type=int, default=0, help="directions per core in the all-core CPU sample (0 = all)")
     ap.add_argument("--dry-run", action="store_true", help="CPU only: spawn ranks, shard the grid, print the line")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="sharded plans: the gathered step stores each rank's envelope rows straight into the "
+                         "root's image (include/dmas.h fused_gather) instead of staged send / recv")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use a sharded plan (NCCL communicator, broadcast, gather) even on one GPU: exercises "
                          "the multi-GPU code path of this script and the library where only one GPU is available")
@@ -380,7 +383,8 @@ def run_ours(args, rank, world, local):
     kw = dict(max_frames=F, lp_taps=LP_TAPS, mf_coeffs=cfg.get("chirp") if args.raw else None,
               delay_interp=1 if args.interp else 0, bf_engine=args.bf_engine, env_engine=args.env_engine)
     if sharded:
-        sb = parallel.ShardedBeamformer(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, device=local, **kw)
+        sb = parallel.ShardedBeamformer(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, device=local,
+                                        fused_gather=1 if args.fused_gather else 0, **kw)
         plan = sb.plan
     else:
         plan = dmas.Plan(cfg["mic_xyz"], dirs, cfg["fs"], cfg["c"], p, T, device=local, **kw)
@@ -509,8 +513,12 @@ def run_ours(args, rank, world, local):
         tg, per_g = timed_steps(step_g, ng)
         gathered = {"value": px_step / (tg / ng * 1e-3), "unit": UNIT, "ms_per_step": tg / ng, "steps": ng,
                     "gather_bytes_to_root_per_step": int(F * (n_dirs_total - plan.n_dirs) * T * 4),
-                    "note": "broadcast + compute + grouped ncclSend/ncclRecv of every chunk's shards into the "
-                            "root's image, overlapped with the next chunk; root link-bound"}
+                    "fused": bool(args.fused_gather),
+                    "note": ("fused: every rank's tensor-core envelope stores its rows straight into the root's "
+                             "image (CUDA IPC mapping, TMA stores), then a stream-ordered barrier"
+                             if args.fused_gather else
+                             "broadcast + compute + grouped ncclSend/ncclRecv of every chunk's shards into the "
+                             "root's image, overlapped with the next chunk; root link-bound")}
         del out_full
 
     # ---- end to end through the public API with host buffers (pinned), copies in the timed region

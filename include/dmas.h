@@ -142,6 +142,13 @@ typedef struct {
                                 ranks are plans of one process, driven from concurrent threads;
                                 the exchange runs as event-ordered device copies with NCCL's
                                 matching and completion semantics)                               */
+  int32_t fused_gather;      /* sharded plans, DMAS_GATHER of envelope-only requests on the
+                                tensor-core envelope: 1 = each rank's envelope kernel stores its
+                                rows straight into the root's images (CUDA IPC mapping of the
+                                root's buffer, TMA stores over NVLink; no staging, no send/recv),
+                                followed by a stream-ordered barrier to the root; 0 = staged
+                                ncclSend / ncclRecv gather (default).  Other requests always take
+                                the staged gather.                                                */
 } dmas_plan_desc;
 
 /* Fill `desc` with defaults (zero geometry; order 2; cf_eps 1e-30; lp 127 taps at 5 kHz;

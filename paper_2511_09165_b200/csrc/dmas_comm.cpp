@@ -13,6 +13,7 @@
 #include <mutex>
 #include <tuple>
 
+#include <cuda.h>
 #include <nccl.h>
 
 namespace dmas {
@@ -160,6 +161,8 @@ struct LoopGroup {
   int ar_count = 0;
   int64_t ar_gen = 0, ar_acc = 0, ar_result = 0;
   std::map<int64_t, LoopMsg> bcast;                                   // by broadcast sequence
+  std::map<int64_t, void*> ptrs;                                      // fused gather: root buffers
+  std::map<int64_t, std::vector<cudaEvent_t>> bars;                   // root barriers: ranks' events
   std::map<std::tuple<int32_t, int32_t, int64_t>, LoopMsg> p2p;       // (src, dst, sequence)
 };
 std::mutex g_loop_mu;
@@ -173,6 +176,9 @@ struct Comm {
   int32_t n_ranks = 1, rank = 0;
   int64_t bseq = 0;                       // loopback: broadcasts issued
   std::map<int32_t, int64_t> sseq, rseq;  // loopback: sends to / receives from each peer
+  int64_t mseq = 0, barseq = 0;           // loopback: root-buffer exchanges / root barriers
+  void* xbuf = nullptr;                   // NCCL: small device buffer for control words
+  std::map<std::string, void*> ipc_open;  // NCCL: root allocations opened by CUDA IPC (non-root ranks)
 };
 
 namespace {
@@ -266,7 +272,110 @@ dmas_status create(const uint8_t id[DMAS_COMM_ID_BYTES], int32_t n_ranks, int32_
     delete c;
     return nccl_fail(r, "ncclCommInitRank", err);
   }
+  if (cudaMalloc(&c->xbuf, 256) != cudaSuccess) {
+    destroy(c);
+    err = "cudaMalloc (control words)";
+    return DMAS_ERR_OOM;
+  }
   *out = c;
+  return DMAS_OK;
+}
+
+namespace {
+// base address of the allocation holding `p` (driver API through the runtime's entry point)
+bool allocation_base(void* p, void** base) {
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<RangeFn>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<void*>(b);
+  return true;
+}
+}  // namespace
+
+dmas_status map_root_buffer(Comm* c, void* root_ptr, int32_t root, void** mapped, cudaStream_t st,
+                            std::string& err) {
+  const bool is_root = c->rank == root;
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    const int64_t seq = c->mseq++;
+    std::unique_lock<std::mutex> lk(g.mu);
+    if (is_root) {
+      g.ptrs[seq] = root_ptr;
+      g.cv.notify_all();
+      *mapped = root_ptr;
+      return DMAS_OK;
+    }
+    g.cv.wait(lk, [&] { return g.ptrs.count(seq) > 0; });
+    *mapped = g.ptrs[seq];
+    return DMAS_OK;
+  }
+  // NCCL: the root exports its allocation (IPC handle + offset), every rank receives it
+  struct Msg {
+    cudaIpcMemHandle_t h;
+    int64_t offset;
+    int64_t ok;
+  } m{};
+  static_assert(sizeof(Msg) <= 256, "control words");
+  if (is_root) {
+    void* base = nullptr;
+    m.ok = allocation_base(root_ptr, &base) && cudaIpcGetMemHandle(&m.h, base) == cudaSuccess;
+    m.offset = m.ok ? (int64_t)((char*)root_ptr - (char*)base) : 0;
+    LOOP_TRY(cudaMemcpyAsync(c->xbuf, &m, sizeof(Msg), cudaMemcpyHostToDevice, st), "fused gather: handle");
+  }
+  NCCL_TRY(api().Broadcast(c->xbuf, c->xbuf, sizeof(Msg), ncclChar, root, c->comm, st), "ncclBroadcast (handle)");
+  LOOP_TRY(cudaMemcpyAsync(&m, c->xbuf, sizeof(Msg), cudaMemcpyDeviceToHost, st), "fused gather: handle");
+  LOOP_TRY(cudaStreamSynchronize(st), "fused gather: handle");
+  if (!m.ok) {
+    err = "fused gather: the root's output buffer cannot be exported by CUDA IPC";
+    return DMAS_ERR_NCCL;
+  }
+  if (is_root) {
+    *mapped = root_ptr;
+    return DMAS_OK;
+  }
+  const std::string key(reinterpret_cast<const char*>(&m.h), sizeof(m.h));
+  auto it = c->ipc_open.find(key);
+  if (it == c->ipc_open.end()) {
+    void* b = nullptr;
+    LOOP_TRY(cudaIpcOpenMemHandle(&b, m.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    it = c->ipc_open.emplace(key, b).first;
+  }
+  *mapped = (char*)it->second + m.offset;
+  return DMAS_OK;
+}
+
+dmas_status root_barrier(Comm* c, int32_t root, cudaStream_t st, std::string& err) {
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    const int64_t seq = c->barseq++;
+    std::unique_lock<std::mutex> lk(g.mu);
+    if (c->rank != root) {
+      cudaEvent_t e = nullptr;
+      LOOP_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "loopback: event");
+      LOOP_TRY(cudaEventRecord(e, st), "loopback: record");
+      g.bars[seq].push_back(e);
+      g.cv.notify_all();
+      return DMAS_OK;
+    }
+    g.cv.wait(lk, [&] { return (int)g.bars[seq].size() >= c->n_ranks - 1; });
+    for (cudaEvent_t e : g.bars[seq]) {
+      LOOP_TRY(cudaStreamWaitEvent(st, e, 0), "loopback: barrier");
+      cudaEventDestroy(e);
+    }
+    g.bars.erase(seq);
+    return DMAS_OK;
+  }
+  NCCL_TRY(api().AllReduce(c->xbuf, c->xbuf, 1, ncclInt32, ncclSum, c->comm, st), "ncclAllReduce (barrier)");
   return DMAS_OK;
 }
 
@@ -276,6 +385,8 @@ void destroy(Comm* c) {
     delete c;
     return;
   }
+  for (auto& kv : c->ipc_open) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(c->xbuf);
   const Api& a = api();
   if (c->comm && a.loaded) {
     ncclResult_t ae = ncclSuccess;

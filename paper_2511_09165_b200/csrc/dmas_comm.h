@@ -38,6 +38,16 @@ void destroy(Comm* c);
 dmas_status broadcast(Comm* c, float* buf, size_t count, int32_t root, cudaStream_t st, std::string& err);
 // all ranks: the minimum over ranks of `v` (ncclAllReduce, blocking; plan time only)
 dmas_status allreduce_min(Comm* c, int64_t* v, cudaStream_t st, std::string& err);
+// Fused gather: every rank gets a pointer through which it writes into the root's buffer
+// `root_ptr` (only read on the root): the root's own pointer on the root; with NCCL the root's
+// allocation exported by CUDA IPC (broadcast over the communicator, opened once per allocation and
+// cached); with the loopback transport the pointer itself.  Collective, blocks on the host.
+dmas_status map_root_buffer(Comm* c, void* root_ptr, int32_t root, void** mapped, cudaStream_t st,
+                            std::string& err);
+// Stream-ordered barrier: the root's `st` does not proceed past this point before every rank's
+// work enqueued on its `st` before the call is complete (ncclAllReduce of one word; loopback:
+// events).  Collective.
+dmas_status root_barrier(Comm* c, int32_t root, cudaStream_t st, std::string& err);
 // execute a gather schedule (grouped ncclSend / ncclRecv, cudaMemcpyAsync for COPY)
 dmas_status run_gather(Comm* c, const std::vector<dmas_xfer>& xs, const float* shard, float* dst, cudaStream_t st,
                        std::string& err);

@@ -194,6 +194,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                "r"(y), "r"(z), "r"(smem_u32(src))
                : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int x, int y, int z, int w) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+               "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(src))
+               : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_NONE, version 1 (sm_100).
@@ -295,7 +300,10 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 12
 __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constant__ CUtensorMap in_map,
                                                            const __grid_constant__ CUtensorMap out_map,
                                                            int64_t rows, int32_t nb,
-                                                           const __grid_constant__ LpTaps127 taps, int32_t L) {
+                                                           const __grid_constant__ LpTaps127 taps, int32_t L,
+                                                           int64_t out_rpf) {
+  // out_rpf > 0: the output map is 4D [frames][out_rpf rows][nb][32] with its own frame stride (a
+  // sharded plan's fused gather writes its rows straight into the root's whole image)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t stage_full[NSTAGE], stage_empty[NSTAGE];
@@ -507,11 +515,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       named_bar(1, 32 * EPIW);
       if (et == 0) {
-        tma_store_3d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)tile_row(jj));
+        const int64_t row = tile_row(jj);
+        if (out_rpf > 0)
+          tma_store_4d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)(row % out_rpf),
+                       (int)(row / out_rpf));
+        else
+          tma_store_3d(&out_map, smem + OFF_OUT + ob * OUT_BYTES, 0, tile_blk(jj), (int)row);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (et == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (out_rpf > 0) __threadfence_system();     // the stores may target a peer GPU's image
+    }
   }
 #ifdef DMAS_TC_PROFILE
   if (lane == 0 && blockIdx.x < 148) {
@@ -560,6 +576,21 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t nb
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [frames][rpf rows][nb][32] view of rows that sit `frame_rows` rows apart per frame
+static bool make_map_4d(CUtensorMap* m, const float* base, int64_t frames, int64_t rpf, int64_t frame_rows,
+                        int64_t nb) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)BLK, (cuuint64_t)nb, (cuuint64_t)rpf, (cuuint64_t)frames};
+  const cuuint64_t strides[3] = {(cuuint64_t)ROW_BYTES, (cuuint64_t)nb * ROW_BYTES,
+                                 (cuuint64_t)frame_rows * nb * ROW_BYTES};
+  const cuuint32_t box[4] = {(cuuint32_t)BLK, (cuuint32_t)TILE_BLOCKS, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace tc
 
 bool envelope_tc_supported(int64_t T) { return T % tc::BLK == 0 && tc::encode_fn() != nullptr; }
@@ -575,14 +606,18 @@ cudaError_t envelope_tc_configure() {
 }
 
 cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
-                               int sm_count, cudaStream_t st) {
+                               int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
   const int64_t nb = T / tc::BLK;
   CUtensorMap in_map, out_map;
-  if (!tc::make_map(&in_map, y, rows, nb, tc::IN_BLOCKS) || !tc::make_map(&out_map, out, rows, nb, tc::TILE_BLOCKS))
+  if (!tc::make_map(&in_map, y, rows, nb, tc::IN_BLOCKS)) return cudaErrorInvalidValue;
+  const bool strided = out_rows_per_frame > 0;
+  if (strided ? !tc::make_map_4d(&out_map, out, rows / out_rows_per_frame, out_rows_per_frame, out_frame_rows, nb)
+              : !tc::make_map(&out_map, out, rows, nb, tc::TILE_BLOCKS))
     return cudaErrorInvalidValue;
   const int64_t tiles = rows * ((nb + tc::TILE_BLOCKS - 1) / tc::TILE_BLOCKS);
   const int64_t grid = tiles < sm_count ? tiles : sm_count;
-  tc::k_envelope_tc<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(in_map, out_map, rows, (int32_t)nb, taps, L);
+  tc::k_envelope_tc<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(in_map, out_map, rows, (int32_t)nb, taps, L,
+                                                                        strided ? out_rows_per_frame : 0);
   return cudaGetLastError();
 }
 

@@ -143,6 +143,7 @@ struct dmas_plan_s {
   float* d_gst[2] = {nullptr, nullptr};   // gather staging (the rank's shard of one chunk)
   size_t gst_cap = 0;
   bool status_exchanged = false;      // plan-time allreduce done (bail must not join it again)
+  bool fused_gather = false;          // DMAS_GATHER of tensor-core envelopes: store into the root's image
 
   // timing
   bool timing = false;
@@ -271,6 +272,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
   if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
   if (d->bf_engine < 0 || d->bf_engine > 1) return fail(DMAS_ERR_INVALID, "bf_engine not in {0, 1}");
+  if (d->fused_gather < 0 || d->fused_gather > 1) return fail(DMAS_ERR_INVALID, "fused_gather not in {0, 1}");
   if (d->delay_interp < 0 || d->delay_interp > 1) return fail(DMAS_ERR_INVALID, "delay_interp not in {0, 1}");
   if (d->mf_taps < 0 || d->mf_taps > dmas::MF_MAX_TAPS) return fail(DMAS_ERR_INVALID, "mf_taps not in [0, 16384]");
   if (d->mf_taps > 0 && !d->mf_coeffs) return fail(DMAS_ERR_NULL, "mf_coeffs is NULL");
@@ -304,7 +306,7 @@ dmas_status validate(const dmas_plan_desc* d) {
 // Enqueue one chunk of frames: roots -> beamform -> envelopes.  `sig` / `outs_raw` / `outs_env`
 // already point at the chunk's first frame.
 dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* const* raw_dst,
-                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st) {
+                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st, int64_t env_frame_rows = 0) {
   // DAS-only requests on the LDS.64 path sum the samples themselves: identity plane (order 1), no
   // roots (the kernel selects its DAS-only variant on the same condition, dmas_kernels.cu)
   Nvtx range("dmas chunk");
@@ -351,9 +353,12 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
     const float* y = raw_dst[k];
     float* o = env_dst[k];
     const bool aligned16 = ((uintptr_t)y % 16 == 0) && ((uintptr_t)o % 16 == 0);
+    if (env_frame_rows > 0 && !(p->lp_tc && aligned16))
+      return fail(DMAS_ERR_CUDA, "internal: fused gather without the tensor-core envelope");
     if (p->lp_tc && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, es, [&] {
-        return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->sm_count, es);
+        return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->sm_count, es,
+                                        env_frame_rows > 0 ? p->n_dirs : 0, env_frame_rows);
       }));
     } else if (p->lp_fast && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, es, [&] { return dmas::launch_envelope_lp127(y, o, rows, p->T, p->lp127, es); }));
@@ -389,7 +394,7 @@ dmas_status check_what(dmas_plan_s* p, uint32_t what, uint32_t& raw_k, uint32_t&
 dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_frames, float* const* outs,
                             uint32_t raw_k, uint32_t env_k, uint32_t flags, cudaStream_t st) {
   const bool sharded = p->comm != nullptr;
-  const bool gather = sharded && (flags & DMAS_GATHER);
+  bool gather = sharded && (flags & DMAS_GATHER);
   const bool bcast = sharded && !(flags & DMAS_SIGNALS_RESIDENT);
   const bool is_root = p->rank == p->root;
   // requested outputs in `outs` order: raw kinds, then envelope kinds, in bit order
@@ -425,6 +430,22 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     const size_t fit = (sharded ? p->x_scratch_cap : p->scratch_cap) / (frame_img * n_scratch);
     if (fit < 1) return fail(DMAS_ERR_CUDA, "internal: envelope scratch smaller than one frame");
     chunk = (int32_t)std::min<size_t>((size_t)chunk, fit);
+  }
+  // fused gather: an envelope-only request on the tensor-core envelope, so the last kernel of every
+  // output can store its rows straight into the root's image (include/dmas.h fused_gather).  The
+  // condition is the same on every rank; the root's buffers are exchanged (collectively) and every
+  // rank checks the 16-byte alignment TMA needs on the pointer it received, so all ranks agree.
+  bool fused = gather && p->fused_gather && raw_k == 0 && p->lp_tc && (p->T_out * sizeof(float)) % 16 == 0;
+  void* mapped[2 * dmas::N_KINDS] = {};
+  if (fused) {
+    std::string err;
+    for (int i = 0; i < n; ++i) {
+      dmas_status rc = dmas::comm::map_root_buffer(p->comm, is_root ? o[i].user : nullptr, p->root, &mapped[i],
+                                                   p->cs, err);
+      if (rc != DMAS_OK) return fail(rc, err);
+      fused = fused && ((uintptr_t)mapped[i] % 16 == 0);
+    }
+    if (fused) gather = false;                        // no staging, no send / recv
   }
   if (gather) {
     size_t per_frame = 0;
@@ -472,14 +493,16 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     float* raw_dst[dmas::N_KINDS] = {};
     float* env_dst[dmas::N_KINDS] = {};
     for (int i = 0; i < n; ++i) {
-      float* dst = gather ? p->d_gst[c & 1] + o[i].stage_off : o[i].user + (size_t)f0 * p->n_dirs * o[i].row;
+      float* dst = fused    ? static_cast<float*>(mapped[i]) + ((size_t)f0 * p->n_dirs_total + p->dir0) * o[i].row
+                   : gather ? p->d_gst[c & 1] + o[i].stage_off
+                            : o[i].user + (size_t)f0 * p->n_dirs * o[i].row;
       (o[i].env ? env_dst : raw_dst)[o[i].k] = dst;
     }
     int s = 0;
     for (int k = 0; k < dmas::N_KINDS; ++k)
       if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
     const float* sig = signals + (size_t)f0 * p->n_mics * p->T_in;
-    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st);
+    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, fused ? p->n_dirs_total : 0);
     if (rc != DMAS_OK) return rc;
     if (gather) {
       Nvtx r("dmas gather");
@@ -498,6 +521,14 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
       rc = issue_bcast(c + 2);
       if (rc != DMAS_OK) return rc;
     }
+  }
+  if (fused) {
+    // the root's stream must not run ahead of the other ranks' stores into its images
+    CUDA_TRY(cudaEventRecord(p->ev_x0, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->cs, p->ev_x0, 0));
+    std::string err;
+    dmas_status rc = dmas::comm::root_barrier(p->comm, p->root, p->cs, err);
+    if (rc != DMAS_OK) return fail(rc, err);
   }
   if (sharded) {
     CUDA_TRY(cudaEventRecord(p->ev_x1, p->cs));
@@ -567,6 +598,7 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
   p->rank = sharded ? desc->rank : 0;
   p->root = sharded ? desc->root : 0;
   p->n_local_max = (full_desc->n_dirs + n_ranks - 1) / n_ranks;
+  p->fused_gather = sharded && full_desc->fused_gather == 1;
   p->T = desc->n_samples;
   p->order = desc->order;
   p->max_frames = desc->max_frames;

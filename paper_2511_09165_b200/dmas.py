@@ -73,6 +73,7 @@ class dmas_plan_desc(ctypes.Structure):
         ("rank", ctypes.c_int32),
         ("root", ctypes.c_int32),
         ("comm_id", ctypes.POINTER(ctypes.c_uint8)),
+        ("fused_gather", ctypes.c_int32),
     ]
 
 
@@ -207,7 +208,8 @@ class Plan:
                  lp_cutoff_hz: float = 5000.0, bp_coeffs: Optional[Sequence[float]] = None, env_decim: int = 1,
                  device: int = -1, scratch_bytes: int = 0, env_engine: int = 0,
                  mf_coeffs: Optional[Sequence[float]] = None, delay_interp: int = 0, bf_engine: int = 0,
-                 n_ranks: int = 0, rank: int = 0, root: int = 0, comm_id: Optional[bytes] = None):
+                 n_ranks: int = 0, rank: int = 0, root: int = 0, comm_id: Optional[bytes] = None,
+                 fused_gather: int = 0):
         self._h = ctypes.c_void_p()
         self._keep = []
         mic = _f64(mic_xyz, 3)
@@ -246,6 +248,7 @@ class Plan:
             self._keep.append(cid)
             d.comm_id = ctypes.cast(cid, ctypes.POINTER(ctypes.c_uint8))
         d.n_ranks, d.rank, d.root = int(n_ranks), int(rank), int(root)
+        d.fused_gather = int(fused_gather)
         self._keep += [mic, dirs]
         _check(lib.dmas_plan(ctypes.byref(d), ctypes.byref(self._h)))
         info = dmas_plan_info()

@@ -606,8 +606,9 @@ def test_linear_presteer_with_matched_filter_and_slices(dm):
     assert np.max(np.abs(r - ref)) <= 1e-5 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("fused", [0, 1])
 @pytest.mark.parametrize("what_name", ["env_all", "raw_env_mix"])
-def test_sharded_plan_one_rank_bitwise(dm, what_name):
+def test_sharded_plan_one_rank_bitwise(dm, what_name, fused):
     """A one-rank sharded plan (n_ranks = 1 with an NCCL comm id: the exchange code runs on one GPU --
     the communicator, the in-place ncclBroadcast per chunk, the comm-stream ordering, the gather
     staging and the gather schedule's local copies) returns images bitwise equal to a plain plan's:
@@ -622,7 +623,8 @@ def test_sharded_plan_one_rank_bitwise(dm, what_name):
     args = (cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], 3, cfg["T"])
     plain = dm.Plan(*args, max_frames=5, scratch_bytes=1)       # 1 frame per chunk (5 envelope-only kinds)
     ref = {k: v.cpu().numpy() for k, v in plain.beamform(x, what).items()}
-    sp = dm.Plan(*args, max_frames=5, scratch_bytes=1, n_ranks=1, rank=0, root=0, comm_id=dm.comm_id())
+    sp = dm.Plan(*args, max_frames=5, scratch_bytes=1, n_ranks=1, rank=0, root=0, comm_id=dm.comm_id(),
+                 fused_gather=fused)
     assert sp.sharded and sp.info["n_dirs_total"] == len(cfg["dirs"]) and sp.info["dir_begin"] == 0
     assert np.array_equal(sp.delay_table(), plain.delay_table())
     resident = sp.beamform(x.clone(), what)

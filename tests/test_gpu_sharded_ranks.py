@@ -52,9 +52,13 @@ def _run_ranks(world, fn):
     return out
 
 
+@pytest.mark.parametrize("fused", [0, 1])
 @pytest.mark.parametrize("world,root", [(2, 0), (3, 0), (3, 2)])
 @pytest.mark.parametrize("what_name", ["env_all", "raw_env_mix"])
-def test_sharded_ranks_bitwise(dm, world, root, what_name):
+def test_sharded_ranks_bitwise(dm, world, root, what_name, fused):
+    """fused = 1: envelope-only gathers store each rank's rows straight into the root's images from
+    the tensor-core envelope kernel (include/dmas.h fused_gather); raw + envelope requests fall back
+    to the staged gather."""
     import torch
     cfg = gen.config("C3")
     sig = np.concatenate([cfg["signals"], gen.random_signals(4, 32, cfg["T"], seed=57)])     # 5 frames
@@ -67,7 +71,7 @@ def test_sharded_ranks_bitwise(dm, world, root, what_name):
     cid = dm.loopback_comm_id()
     n_dirs = len(cfg["dirs"])
     plans = _run_ranks(world, lambda r: dm.Plan(*args, max_frames=5, scratch_bytes=1, n_ranks=world, rank=r,
-                                                root=root, comm_id=cid, device=0))
+                                                root=root, comm_id=cid, device=0, fused_gather=fused))
     for r, p in enumerate(plans):
         assert p.sharded and p.info["n_dirs_total"] == n_dirs
         assert (p.dir_begin, p.dir_begin + p.n_dirs) == dm.shard_range(n_dirs, world, r)
