@@ -180,17 +180,39 @@ cudaError_t launch_mf_roots(int order, const float* raw, int64_t T_raw, const fl
   return cudaGetLastError();
 }
 
+// Dynamic shared-memory opt-in.  cudaFuncSetAttribute is process-wide per kernel, so every
+// configure call raises the limit to the most the kernel can take (the device's opt-in maximum
+// less its static shared memory) instead of this plan's own need: a later (or concurrent,
+// another thread's) plan with a smaller window must never lower the limit under an earlier
+// plan's launches.  The launch's own smem argument still decides occupancy.
+static cudaError_t smem_optin(int need, int* optin) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess && need > *optin) e = cudaErrorInvalidValue;
+  return e;
+}
+
+template <typename K>
+static cudaError_t set_smem_max(K* kernel, int optin) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
 cudaError_t mf_configure(int32_t Lp) {
-  const int smem = (2 * Lp + MF_T) * (int)sizeof(float);
+  int smem = 0;
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_mf_roots<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  return cudaFuncSetAttribute(k_mf_roots<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if ((e = smem_optin((2 * Lp + MF_T) * (int)sizeof(float), &smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<1>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<2>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<3>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<4>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<5>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<6>, smem))) return e;
+  if ((e = set_smem_max(k_mf_roots<7>, smem))) return e;
+  return set_smem_max(k_mf_roots<8>, smem);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -998,35 +1020,33 @@ size_t beamform_lds64_smem_bytes(int32_t n_mics, int32_t W, bool interp, int32_t
 template <int P>
 static cudaError_t configure_order(int bytes) {
   cudaError_t e;
-  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 4, true>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform<P, 31, true>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 4, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 31, false>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_mg<P, 4, true>, attr, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform_mg<P, 31, true>, attr, bytes);
+  if ((e = set_smem_max(k_beamform<P, 4, false>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform<P, 31, false>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform<P, 4, true>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform<P, 31, true>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_mg<P, 4, false>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_mg<P, 31, false>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_mg<P, 4, true>, bytes))) return e;
+  return set_smem_max(k_beamform_mg<P, 31, true>, bytes);
 }
 
 template <int P>
 static cudaError_t configure_order_lds64(int bytes) {
   cudaError_t e;
-  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false, 8>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, false, 8>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, true, 8>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 31, true, 8>, attr, bytes))) return e;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<P, 4, false, 4>, attr, bytes))) return e;
-  return cudaFuncSetAttribute(k_beamform_lds64<P, 31, false, 4>, attr, bytes);
+  if ((e = set_smem_max(k_beamform_lds64<P, 4, false, 8>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_lds64<P, 31, false, 8>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_lds64<P, 4, true, 8>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_lds64<P, 31, true, 8>, bytes))) return e;
+  if ((e = set_smem_max(k_beamform_lds64<P, 4, false, 4>, bytes))) return e;
+  return set_smem_max(k_beamform_lds64<P, 31, false, 4>, bytes);
 }
 
 cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int32_t kt, int32_t psi) {
-  const int bytes = (int)beamform_lds64_smem_bytes(n_mics, W, interp, kt, psi);
+  int bytes = 0;
   cudaError_t e;
-  const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<2, 1, false, 8>, attr, bytes))) return e;   // DAS-only
-  if ((e = cudaFuncSetAttribute(k_beamform_lds64<2, 1, false, 4>, attr, bytes))) return e;
+  if ((e = smem_optin((int)beamform_lds64_smem_bytes(n_mics, W, interp, kt, psi), &bytes))) return e;
+  if ((e = set_smem_max(k_beamform_lds64<2, 1, false, 8>, bytes))) return e;   // DAS-only
+  if ((e = set_smem_max(k_beamform_lds64<2, 1, false, 4>, bytes))) return e;
   if ((e = configure_order_lds64<2>(bytes))) return e;
   if ((e = configure_order_lds64<3>(bytes))) return e;
   if ((e = configure_order_lds64<4>(bytes))) return e;
@@ -1037,8 +1057,9 @@ cudaError_t beamform_lds64_configure(int32_t n_mics, int32_t W, bool interp, int
 }
 
 cudaError_t beamform_configure(int32_t n_mics, int32_t W, bool interp, int32_t mg) {
-  const int bytes = (int)beamform_smem_bytes(n_mics, W, interp, mg);
+  int bytes = 0;
   cudaError_t e;
+  if ((e = smem_optin((int)beamform_smem_bytes(n_mics, W, interp, mg), &bytes))) return e;
   if ((e = configure_order<2>(bytes))) return e;
   if ((e = configure_order<3>(bytes))) return e;
   if ((e = configure_order<4>(bytes))) return e;
@@ -1240,8 +1261,10 @@ cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, in
   const int c = (L - 1) / 2, cb = Lb > 0 ? (Lb - 1) / 2 : 0;
   const int64_t nb = (int64_t)(ENV_GEN_T - 1) * decim + 2 * c + 1;
   const size_t smem = (size_t)(nb + (Lb > 0 ? nb + 2 * cb : 0)) * sizeof(float);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_envelope_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {                               // opt-in maximum: see smem_optin
+    int bytes = 0;
+    cudaError_t e = smem_optin((int)smem, &bytes);
+    if (e == cudaSuccess) e = set_smem_max(k_envelope_generic, bytes);
     if (e != cudaSuccess) return e;
   }
   dim3 grid((unsigned)rows, (unsigned)((T_out + ENV_GEN_T - 1) / ENV_GEN_T));

@@ -434,6 +434,24 @@ def test_calls_do_not_allocate_and_graph_replay(dm):
         assert np.array_equal(o.cpu().numpy(), e)
 
 
+def test_plans_with_different_windows_coexist(dm):
+    """A later plan with a smaller shared-memory window must not break an earlier plan's launches
+    (the kernels' dynamic-smem limit is process-wide; dmas_kernels.cu smem_optin)."""
+    import torch
+    big = dm.Plan(gen.disk_array(64, 0.10, 4e-3, seed=11), gen.az_el_grid(16, 90.0, 16, 60.0), gen.FS,
+                  gen.C_SOUND, 3, 2048, max_frames=1)
+    xb = torch.from_numpy(gen.random_signals(1, 64, 2048, seed=3)).cuda()
+    what = dm.RAW(dm.KIND_ALL) | dm.ENV(dm.KIND_ALL)
+    first = {k: v.cpu().numpy() for k, v in big.beamform(xb, what).items()}
+    small = dm.Plan(gen.ula(8), gen.az_grid_deg(np.arange(-90, 91, 2)), gen.FS, gen.C_SOUND, 3, 1024, max_frames=1)
+    small.beamform(torch.from_numpy(gen.random_signals(1, 8, 1024, seed=4)).cuda(), what)
+    again = {k: v.cpu().numpy() for k, v in big.beamform(xb, what).items()}
+    torch.cuda.synchronize()
+    assert big.n_mics * big.info["window"] > small.n_mics * small.info["window"]
+    for k in first:
+        assert np.array_equal(first[k], again[k]), k
+
+
 def test_timing_and_launch_counter(dm):
     import torch
     plan = dm.Plan(gen.ula(8), gen.az_grid_deg(np.arange(-90, 91, 2)), gen.FS, gen.C_SOUND, 2, 1024, max_frames=4)

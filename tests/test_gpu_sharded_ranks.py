@@ -39,6 +39,10 @@ def _run_ranks(world, fn):
                 out[r] = fn(r)
                 s.synchronize()
         except Exception as e:          # noqa: BLE001 -- reported below
+            import sys
+            import traceback
+            print(f"rank {r} failed: {e!r}", file=sys.stderr, flush=True)
+            traceback.print_exc()
             errs.append((r, e))
 
     th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
@@ -53,7 +57,7 @@ def _run_ranks(world, fn):
 
 
 @pytest.mark.parametrize("fused", [0, 1])
-@pytest.mark.parametrize("world,root", [(2, 0), (3, 0), (3, 2)])
+@pytest.mark.parametrize("world,root", [(2, 0), (3, 0), (3, 2), (8, 5)])
 @pytest.mark.parametrize("what_name", ["env_all", "raw_env_mix"])
 def test_sharded_ranks_bitwise(dm, world, root, what_name, fused):
     """fused = 1: envelope-only gathers store each rank's rows straight into the root's images from
