@@ -73,8 +73,9 @@ def parse():
     ap.add_argument("--mode", choices=["dirshard", "weak"], default="dirshard")
     ap.add_argument("--bf-engine", type=int, choices=[0, 1], default=0,
                     help="beamform kernel: 0 auto (LDS.64 kernel where it fits), 1 classic k_beamform (comparison)")
-    ap.add_argument("--env-engine", type=int, choices=[0, 1], default=0,
-                    help="envelope low-pass: 0 tcgen05 (BF16 split), 1 the FP32 FIR")
+    ap.add_argument("--env-engine", type=int, choices=[0, 1, 2], default=0,
+                    help="envelope low-pass: 0 tcgen05 (BF16 split written by the beamform), 1 the FP32 FIR, "
+                         "2 tcgen05 on the fp32 image (split inside the envelope kernel; comparison)")
     ap.add_argument("--interp", action="store_true",
                     help="linear-interpolation pre-steering (fractional delays, roots on the fly; NEXT-2)")
     ap.add_argument("--raw", action="store_true",
@@ -495,7 +496,8 @@ def run_ours(args, rank, world, local):
             "envelope": {"avg_ms": env_avg, "launches": env_n, "share": env_ms / total_ms, "bound": "hbm",
                          "GB_s": env_gbs, "hbm_frac": env_gbs / hbm_peak, "algorithmic_bytes_per_px": 8,
                          "Gpx_s": px_launch_env / (env_avg * 1e-3) / 1e9 if env_n else None,
-                         "engine": "FP32 FIR" if args.env_engine else "tcgen05 BF16x3",
+                         "engine": "FP32 FIR" if args.env_engine == 1 else "tcgen05 BF16x3" + (
+                             " (fp32 input, in-kernel split)" if args.env_engine == 2 else " (pre-split input)"),
                          "ncu_dram_bytes_per_launch": prof.get("k_envelope", {}).get("dram_bytes_per_launch"),
                          "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"},
             "signed_roots": {"avg_ms": rt_ms / max(1, rt_n), "launches": rt_n, "share": rt_ms / total_ms}}}
@@ -581,9 +583,9 @@ def run_ours(args, rank, world, local):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if args.mode == "dirshard" else "weak", "vs_baseline": None,
-            "dtype": "f32" + ("" if args.env_engine else "+bf16x3(tcgen05 envelope)"),
+            "dtype": "f32" + ("" if args.env_engine == 1 else "+bf16x3(tcgen05 envelope)"),
             "dtype_detail": ("beamform A2-A4 in FP32 (delay table A1 in FP64); " +
-                             ("envelope FP32 FIR" if args.env_engine else ENV_PRECISION)),
+                             ("envelope FP32 FIR" if args.env_engine == 1 else ENV_PRECISION)),
             "data": "synthetic (seeded eRTIS-like point-reflector echoes, matched-filtered; workloads/gen.py)",
             "config": config_dict(args, world), "beamform_kernel": bf_name,
             "frames_per_s": F * (world if args.mode == "weak" else 1) / (ms * 1e-3),

@@ -102,7 +102,11 @@ typedef struct {
   int32_t env_engine;        /* 0 = auto: tensor-core (tcgen05) low-pass with a 3-pass BF16 split
                                 (error <= ~4.6e-5 of the envelope) when lp_taps <= 127, no
                                 band-pass, R == 1, T % 32 == 0 and 16-byte aligned buffers,
-                                else the FP32 FIR; 1 = always the FP32 FIR                      */
+                                else the FP32 FIR.  For envelope-only kinds the beamform then
+                                writes |y| already split into BF16 hi / lo (same 4 B per pixel)
+                                and the envelope reads it without a conversion pass (identical
+                                values).  1 = always the FP32 FIR; 2 = the tensor-core envelope
+                                on the fp32 raw image (conversion inside the envelope kernel) */
   /* Optional matched filter (pulse compression; NEXT-1).  When mf_taps > 0 the
      signals given to dmas_beamform* are RAW recordings of n_samples + mf_taps - 1 samples per
      channel, and each channel is first correlated with the emitted signal:

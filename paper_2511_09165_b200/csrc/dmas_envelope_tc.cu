@@ -16,38 +16,32 @@
 // inside the 1e-4 parity bar in the worst case (measured: ~2e-6 on C1-C5 images; the adversarial
 // rows of tests/test_gpu_parity.py::test_envelope_tc_adversarial_split_inputs).
 //
-// Why this shape (measured on B200): every tcgen05.mma with N <= 64 costs >= 44 cycles, and in SS
-// mode the 4 KB A operand was re-read from shared memory by every MMA.  So A lives in TMEM (TS
-// mode: 5 block-shifted copies per split, double-buffered) and only the H_q operand is read from
-// shared memory.  Per (shift, K-step) two MMAs: D[0:64] += A_hi x [H_hi | H_lo] (N = 64) and
-// D[0:32] += A_lo x H_hi (N = 32), 20 per tile; the epilogue adds D[0:32] + D[32:64].
+// Operand layout: each sample becomes the BF16 pair (hi, lo) in one 32-bit word (split_pair), so a
+// block row is 32 pairs = 64 bf16 = 128 B, laid out exactly like the fp32 row it came from.  The
+// MMA takes that row as an interleaved K = 64 operand: with B1[2k] = B1[2k+1] = H_hi[k] and
+// B2[2k] = H_lo[k], B2[2k+1] = 0, one N = 64 MMA over [B1 | B2] gives D[0:32] = hi*H_hi + lo*H_hi
+// and D[32:64] = hi*H_lo; the epilogue adds the halves.  4 K-steps x 5 shifts = 20 MMAs per tile
+// (the same count as separate hi / lo operands: at N <= 64 a tcgen05.mma costs its issue, ~44
+// cycles, not its MACs).  The pair layout lets the producer of the image write the operand itself:
+// for envelope-only requests the beamform epilogue stores split pairs instead of fp32 (PS = true:
+// no conversion here at all); on an fp32 image (raw + envelope requests) converter warps split the
+// staged tile in place.  Both routes feed identical words to identical MMAs: bitwise-equal outputs.
 //
-// The block-shifted A copies: the converted tile is stored "column-chunk major" -- 16-byte chunk j
-// of every block row r at j * CLBO + 16 r -- so rows are 16 B apart everywhere and the canonical
-// no-swizzle K-major layout (SBO = 128 B per 8 rows) describes the tile starting at ANY row.
-// Shift 0 is copied into TMEM by the tensor core itself (tcgen05.cp 128x256b through a descriptor
-// whose start moves by q rows, issued by the MMA thread ahead of its MMAs: same-thread tcgen05.cp
-// and tcgen05.mma execute in issue order); shifts 1..4 by 4 copy warps (LDS.128 + tcgen05.st).
-// Measured per 16-frame C5 chunk (tools/time_variants.py, profiles/r02/envelope_variants.json):
-// all 5 shifts by copy warps 1.63 ms, 1 by tcgen05.cp 1.58 ms, 2: 1.64, 3: 1.72, all 5: 2.21
-// (tcgen05.cp moves ~40 B/clk/SM and queues in front of the MMAs).  The converters load their
-// whole share of a stage before converting (round 1 converted item by item: the converter warps
-// were ~85% busy on load latency).  Role profile after both changes (DMAS_TC_PROFILE): MMA issuer
-// ~75% busy, epilogue ~75%, converters ~60%, copy warps ~55%; HBM at ~0.85 of the copy bandwidth.
+// Data movement: 3D TMA tensor maps view a [rows][T] image (fp32 or pairs, 4 B per sample) as
+// [rows][T/32 blocks][32] with 128-byte swizzle.  The load box is 132 blocks (the tile + a 2-block
+// halo each side; blocks outside the row are zero-filled by TMA = zero pairs), the store box 128
+// blocks (blocks past the row end are clipped).  Requires T % 32 == 0 and 16-byte aligned buffers.
+// The block-shifted A copies live in TMEM (TS mode; A_q = rows q .. q + 127 of the staged tile):
+// copy warps read them from the swizzled stage (conflict-free LDS.128) and store them with
+// tcgen05.st; only the taps are read from shared memory by the MMAs.
 //
-// Data movement: 3D TMA tensor maps view a [rows][T] image as [rows][T/32 blocks][32 samples]
-// with 128-byte swizzle.  The load box is 132 blocks (the tile + a 2-block halo each side; blocks
-// outside the row are zero-filled by TMA), the store box 128 blocks (blocks past the row end are
-// clipped).  Requires T % 32 == 0 and 16-byte aligned buffers (the plan falls back otherwise).
-//
-// Per CTA (persistent, 1 CTA / SM, warp-specialised roles linked by mbarriers, every stage
-// double- or quad-buffered so the roles run concurrently):
-//   warps 0..3      epilogue: tcgen05.ld (2 x 32 columns) -> add -> clamp -> swizzled smem -> TMA store
-//   warps 4..7      copy: block shifts 1..4 of each TMEM lane quarter (LDS.128 + tcgen05.st.x16)
-//   warps 8..15     converters: stage -> |.| -> BF16 hi / lo, once per sample, column-chunk major
-//   warp 16         MMA issuer (one elected lane): 4 tcgen05.cp (shift 0) + 20 tcgen05.mma per tile
-//                   into one of two TMEM accumulators
-//   warp 17 lane 0  TMA producer: 4-slot ring of input tiles
+// Per CTA (persistent, 1 CTA / SM, warp-specialised roles linked by mbarriers):
+//   epilogue warps    2 groups of 4 (group g drains accumulator buffer g): tcgen05.ld (2 x 32
+//                     columns) -> add -> clamp -> swizzled smem -> TMA store
+//   copy warps        block shifts 0..4 of each TMEM lane quarter (LDS.128 + tcgen05.st.x32)
+//   converter warps   (fp32 input only) |.| -> BF16 pair, in place in the stage
+//   MMA warp          one elected lane: 20 tcgen05.mma per tile into one of two TMEM accumulators
+//   TMA warp, lane 0  producer: NSTAGE-slot ring of input tiles
 
 #include <cstdint>
 #include <cuda.h>
@@ -59,85 +53,75 @@
 namespace dmas {
 namespace tc {
 
-constexpr int BLK = 32;                    // samples per block (MMA N; K per shift)
+constexpr int BLK = 32;                    // samples per block (the N of one output block)
 constexpr int TILE_BLOCKS = 128;           // MMA M: blocks per tile
 constexpr int HALO = 2;                    // block shifts q in [-2, 2]
 constexpr int NQ = 2 * HALO + 1;
 constexpr int IN_BLOCKS = TILE_BLOCKS + 2 * HALO;   // 132 rows per input box
-constexpr int ROW_BYTES = BLK * 4;                  // 128 B per block row (fp32)
+constexpr int ROW_BYTES = BLK * 4;                  // 128 B per block row (fp32 or bf16 pairs)
 constexpr int STAGE_BYTES = 17408;                  // 132 * 128 rounded up to 1024 (swizzle atom)
 constexpr int OUT_BYTES = TILE_BLOCKS * ROW_BYTES;  // 16384
 #ifndef DMAS_TC_NSTAGE
-#define DMAS_TC_NSTAGE 4
+#define DMAS_TC_NSTAGE 6
 #endif
 constexpr int NSTAGE = DMAS_TC_NSTAGE;
 #ifndef DMAS_TC_NOUT
 #define DMAS_TC_NOUT 4
 #endif
 constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (TMA stores in flight)
-// block shifts copied into TMEM by tcgen05.cp (shifts 0 .. NCP-1); the others by the copy warps
-#ifndef DMAS_TC_NCP
-#define DMAS_TC_NCP 1
-#endif
-constexpr int NCP = DMAS_TC_NCP;
-static_assert(NCP >= 0 && NCP <= 5, "NCP");
 #ifndef DMAS_TC_COPYW
 #define DMAS_TC_COPYW 4
 #endif
+constexpr int NCOPYW = DMAS_TC_COPYW;               // 4 (one per TMEM lane quarter) or 8 (two per
+static_assert(NCOPYW == 4 || NCOPYW == 8, "COPYW"); // quarter, alternate shifts)
 #ifndef DMAS_TC_CONVW
-#define DMAS_TC_CONVW 8
+#define DMAS_TC_CONVW 4
 #endif
-constexpr int NCOPYW = NCP < 5 ? DMAS_TC_COPYW : 0;  // copy warps: 4 (one per TMEM lane quarter) or 8
-                                                    // (two per quarter, alternate shifts)
-// epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, 16 output columns each)
-#ifndef DMAS_TC_EPIW
-#define DMAS_TC_EPIW 4
+// epilogue groups of 4 warps (one per TMEM lane quarter); with 2 groups, group g drains the tiles
+// of accumulator buffer g, so two tiles' drains (TMEM load -> smem -> TMA store) overlap
+#ifndef DMAS_TC_EPIG
+#define DMAS_TC_EPIG 2
 #endif
-constexpr int EPIW = DMAS_TC_EPIW;
-static_assert(EPIW == 4 || EPIW == 8, "EPIW");
-constexpr int EPI_COLS = BLK * 4 / EPIW;            // output columns per epilogue thread (32 or 16)
-// warp roles
-constexpr int EPI_WARP0 = 0;                        // TMEM accumulator -> clamp -> TMA store
-constexpr int COPY_WARP0 = EPIW;                    // the other shifted A copies (LDS + tcgen05.st)
-constexpr int CONV_WARP0 = COPY_WARP0 + NCOPYW;     // 8 warps: fp32 stage -> bf16 hi / lo buffer
+constexpr int EPIG = DMAS_TC_EPIG;
+static_assert(EPIG == 1 || EPIG == 2, "EPIG");
+constexpr int EPIW = 4 * EPIG;
+static_assert(NOUT % EPIG == 0, "NOUT");
+constexpr int NOUT_G = NOUT / EPIG;                 // output staging buffers per group
+// warp roles (PS = pre-split input: no converter warps)
+constexpr int EPI_WARP0 = 0;
+constexpr int COPY_WARP0 = EPIW;
+constexpr int CONV_WARP0 = COPY_WARP0 + NCOPYW;
 constexpr int CONV_WARPS = DMAS_TC_CONVW;
-constexpr int MMA_WARP = CONV_WARP0 + CONV_WARPS;
-constexpr int TMA_WARP = MMA_WARP + 1;
 constexpr int CONV_THREADS = CONV_WARPS * 32;
-constexpr int THREADS = (TMA_WARP + 1) * 32;
+template <bool PS> __host__ __device__ constexpr int mma_warp() { return CONV_WARP0 + (PS ? 0 : CONV_WARPS); }
+template <bool PS> __host__ __device__ constexpr int tma_warp() { return mma_warp<PS>() + 1; }
+template <bool PS> __host__ __device__ constexpr int threads() { return (tma_warp<PS>() + 1) * 32; }
 
-// H_q^T in shared memory: K-major canonical layout, no swizzle, 8 bf16 per 16-byte core row; per
-// shift q the N rows are [H_q hi (32 rows) | H_q lo (32 rows)], so one N = 64 MMA multiplies A_hi by
-// both halves of the split taps and an N = 32 MMA on the first 32 rows multiplies A_lo by H_hi:
-// 2 MMAs per (shift, K-step) instead of 3 (the instruction issue -- ~44 cycles per tcgen05.mma at
-// N <= 64 -- bounds the tile, ncu/role profile DESIGN.md §6).
-constexpr int BROWS = 2 * BLK;                      // 64 B-operand rows per shift
-constexpr int B_LBO = BROWS * 16;                   // 1024 B between K core columns
-constexpr int B_BYTES = B_LBO * (BLK / 8);          // 4096 B per shift
+// [B1 | B2]^T per shift in shared memory: N = 64 rows x K = 64 (interleaved pairs), K-major
+// canonical layout, no swizzle: 8 bf16 per 16-byte core row, B_LBO between K core columns.
+constexpr int BROWS = 2 * BLK;                      // 64 rows: B1 (0..31), B2 (32..63)
+constexpr int KI = 2 * BLK;                         // 64 interleaved K
+constexpr int B_LBO = BROWS * 16;                   // 1024 B
+constexpr int B_BYTES = B_LBO * (KI / 8);           // 8192 B per shift
 constexpr int K_MMA = 16;
 
-// TMEM columns (fp32 / packed bf16x2): A copies [buf][split][shift] x 16 columns, then D[buf].
-constexpr int A_COLS = 16;                          // 32 bf16 of one block row
-constexpr int A_BUF_COLS = 2 * NQ * A_COLS;         // 160
+// TMEM columns (32-bit): A copies [buf][shift] x 32 columns (one block row of pairs per lane), then D[buf]
+constexpr int A_COLS = BLK;                         // 32 pairs
+constexpr int A_BUF_COLS = NQ * A_COLS;             // 160
 constexpr int D_COL0 = 2 * A_BUF_COLS;              // 320: D[buf] = 64 columns (hi*h_hi + lo*h_hi | hi*h_lo)
 constexpr int D_COLS = 2 * BLK;
 static_assert(D_COL0 + 2 * D_COLS <= 512, "TMEM columns");
 constexpr int TMEM_COLS = 512;
 
-// converted tile, column-chunk major: chunk j (0..3 hi, 4..7 lo; 8 bf16 = samples 8(j%4)..+7 of the
-// block) of block row r (block -2 + r) at j * CLBO + 16 r.  CLBO = 132 rows * 16 B.
-constexpr int CLBO = IN_BLOCKS * 16 + 96;           // 2208 B between chunk columns (== 32 mod 128: a
-                                                    // converter half-warp's 4 chunk stores hit disjoint banks)
-constexpr int CONV_BYTES = (8 * CLBO + 1023) / 1024 * 1024;   // 18432 B (keeps the staging below 1024-aligned)
 constexpr int OFF_STAGE = 0;
-constexpr int OFF_CONV = OFF_STAGE + NSTAGE * STAGE_BYTES;
-constexpr int OFF_OUT = OFF_CONV + 2 * CONV_BYTES;
+constexpr int OFF_OUT = OFF_STAGE + NSTAGE * STAGE_BYTES;
 constexpr int OFF_B = OFF_OUT + NOUT * OUT_BYTES;
 constexpr int SMEM_BYTES = OFF_B + NQ * B_BYTES + 1024;   // + alignment slack
+static_assert(SMEM_BYTES <= 232448 - 256, "shared memory");
 
-// instruction descriptors: D f32, A/B bf16 (kind::f16), K-major, M = 128, N = 32 / 64
+// instruction descriptor: D f32, A/B bf16 (kind::f16), K-major, M = 128, N = 64
 constexpr uint32_t idesc(uint32_t n) { return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24); }
-constexpr uint32_t IDESC32 = idesc(BLK), IDESC64 = idesc(2 * BLK);
+constexpr uint32_t IDESC64 = idesc(2 * BLK);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -217,17 +201,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-// smem -> TMEM copy by the tensor core: 128 rows (lanes) x 256 bits (8 columns) from the matrix
-// the descriptor describes; asynchronous, ordered with this thread's tcgen05.mma
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&v)[4]) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint4 (&v)[8]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
       "r"(v[0].x), "r"(v[0].y), "r"(v[0].z), "r"(v[0].w), "r"(v[1].x), "r"(v[1].y), "r"(v[1].z), "r"(v[1].w),
-      "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z), "r"(v[3].w)
+      "r"(v[2].x), "r"(v[2].y), "r"(v[2].z), "r"(v[2].w), "r"(v[3].x), "r"(v[3].y), "r"(v[3].z), "r"(v[3].w),
+      "r"(v[4].x), "r"(v[4].y), "r"(v[4].z), "r"(v[4].w), "r"(v[5].x), "r"(v[5].y), "r"(v[5].z), "r"(v[5].w),
+      "r"(v[6].x), "r"(v[6].y), "r"(v[6].z), "r"(v[6].w), "r"(v[7].x), "r"(v[7].y), "r"(v[7].z), "r"(v[7].w)
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -244,22 +225,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-template <int N>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[N]) {
-  if constexpr (N == 32) tmem_ld32(taddr, v);
-  else tmem_ld16(taddr, v);
-}
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -270,22 +235,21 @@ __device__ __forceinline__ uint4 lds128u(uint32_t a) {
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
-__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
-  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+__device__ __forceinline__ void sts128u(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
-// BF16 hi / lo split of two non-negative values with integer rounding (round half up on the
-// magnitude; |a - hi| <= 2^-8 |a|, lo = a - hi exact, |lo - bf16(lo)| <= 2^-8 |lo|), packed as bf16x2
-// (first value in the low half).  ALU + FADD only: no F2F on the MIO pipe.
-__device__ __forceinline__ void split2(float a0, float a1, uint32_t& hi2, uint32_t& lo2) {
-  const uint32_t h0 = (__float_as_uint(a0) + 0x8000u) & 0xFFFF0000u;
-  const uint32_t h1 = (__float_as_uint(a1) + 0x8000u) & 0xFFFF0000u;
-  const uint32_t l0 = __float_as_uint(a0 - __uint_as_float(h0)) + 0x8000u;
-  const uint32_t l1 = __float_as_uint(a1 - __uint_as_float(h1)) + 0x8000u;
-  hi2 = __byte_perm(h0, h1, 0x7632);
-  lo2 = __byte_perm(l0, l1, 0x7632);
+// |a| as the BF16 pair (hi, lo) in one 32-bit word, hi in the low half: hi = |a| rounded half up
+// on the magnitude to 8 significant bits (|a| - hi exact, <= 2^-8 |a|), lo = the remainder rounded
+// the same way.  Integer round-and-mask + one FADD: no F2F on the MIO pipe.  The beamform's split
+// epilogue (dmas_kernels.cu split_pair) is this function, bit for bit.
+__device__ __forceinline__ uint32_t split_pair(float a) {
+  const uint32_t b = __float_as_uint(a) & 0x7FFFFFFFu;          // |a| (LOP3, not an FADD on the FMA pipe)
+  const uint32_t h = (b + 0x8000u) & 0xFFFF0000u;
+  const uint32_t l = __float_as_uint(__uint_as_float(b) - __uint_as_float(h)) + 0x8000u;
+  return __byte_perm(h, l, 0x7632);                    // hi in the low half (the lower address)
 }
 // BF16 hi / lo split of one value (raw 16-bit patterns)
 __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) {
@@ -297,17 +261,20 @@ __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) 
 // byte offset of 16-byte chunk `c` of row `r` in a 128-byte-swizzled [rows][128 B] tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-__global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constant__ CUtensorMap in_map,
-                                                           const __grid_constant__ CUtensorMap out_map,
-                                                           int64_t rows, int32_t nb,
-                                                           const __grid_constant__ LpTaps127 taps, int32_t L,
-                                                           int64_t out_rpf) {
+template <bool PS>
+__global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_constant__ CUtensorMap in_map,
+                                                                const __grid_constant__ CUtensorMap out_map,
+                                                                int64_t rows, int32_t nb,
+                                                                const __grid_constant__ LpTaps127 taps, int32_t L,
+                                                                int64_t out_rpf) {
+  // PS: the input holds split pairs already (BeamformArgs::split_mask); else fp32 samples.
   // out_rpf > 0: the output map is 4D [frames][out_rpf rows][nb][32] with its own frame stride (a
   // sharded plan's fused gather writes its rows straight into the root's whole image)
+  constexpr int THREADS = threads<PS>(), MMA_WARP = mma_warp<PS>(), TMA_WARP = tma_warp<PS>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t stage_full[NSTAGE], stage_empty[NSTAGE];
-  __shared__ __align__(8) uint64_t conv_full[2], conv_empty[2], a_full[2], mma_done[2], d_empty[2];
+  __shared__ __align__(8) uint64_t stage_full[NSTAGE], stage_empty[NSTAGE], conv_full[NSTAGE];
+  __shared__ __align__(8) uint64_t a_full[2], mma_done[2], d_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -321,18 +288,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     return (int)((g - (g / tiles_per_row) * tiles_per_row) * TILE_BLOCKS);
   };
 
-  // ---- one-time setup: barriers, TMEM, the constant Toeplitz blocks H_q^T (bf16 hi / lo)
+  // ---- one-time setup: barriers, TMEM, the constant Toeplitz blocks [B1 | B2]^T
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&stage_full[s], 1);
-      mbar_init(&stage_empty[s], CONV_THREADS);
+      mbar_init(&stage_empty[s], 32 * NCOPYW);       // the copy warps' reads
+      mbar_init(&conv_full[s], CONV_THREADS);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&conv_full[b], CONV_THREADS);
-      mbar_init(&conv_empty[b], 1 + 32 * NCOPYW);    // copy warps' reads + the commit after the cps
-      mbar_init(&a_full[b], 32 * NCOPYW > 0 ? 32 * NCOPYW : 1);
+      mbar_init(&a_full[b], 32 * NCOPYW);
       mbar_init(&mma_done[b], 1);
-      mbar_init(&d_empty[b], 32 * EPIW);
+      mbar_init(&d_empty[b], 32 * 4);                // the epilogue group that drains buffer b
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -341,15 +307,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
                  "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // row n, interleaved K index kk = 2k + part: B1 (n < 32) = h_hi at both parts; B2 = h_lo at
+  // part 0, 0 at part 1; tap index j = n' + c - 32 q - k with n' = n mod 32
   const int c = (L - 1) / 2;
-  for (int e = tid; e < NQ * BLK * BLK; e += THREADS) {
-    const int qi = e / (BLK * BLK), r = e - qi * BLK * BLK, n = r / BLK, k = r - n * BLK;
-    const int j = n + c - BLK * (qi - HALO) - k;
+  for (int e = tid; e < NQ * BROWS * KI; e += THREADS) {
+    const int qi = e / (BROWS * KI), r = e - qi * BROWS * KI, n = r / KI, kk = r - n * KI;
+    const int j = (n & (BLK - 1)) + c - BLK * (qi - HALO) - (kk >> 1);
     uint32_t hi = 0, lo = 0;
     if (j >= 0 && j < L) split_bf16(taps.h[j], hi, lo);
-    const uint32_t off = (uint32_t)(qi * B_BYTES + n * 16 + (k >> 3) * B_LBO + (k & 7) * 2);
-    *reinterpret_cast<uint16_t*>(smem + OFF_B + off) = (uint16_t)hi;                 // row n
-    *reinterpret_cast<uint16_t*>(smem + OFF_B + off + BLK * 16) = (uint16_t)lo;      // row 32 + n
+    const uint32_t v = n < BLK ? hi : ((kk & 1) ? 0u : lo);
+    const uint32_t off = (uint32_t)(qi * B_BYTES + n * 16 + (kk >> 3) * B_LBO + (kk & 7) * 2);
+    *reinterpret_cast<uint16_t*>(smem + OFF_B + off) = (uint16_t)v;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -375,12 +343,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     }
   } else if (warp == MMA_WARP) {
     // ================= MMA issuer (whole warp runs the loop so every operand is warp-uniform and
-    // lives in uniform registers; one elected lane issues): 5 shifts x 2 K-steps x 3 passes, TS mode
+    // lives in uniform registers; one elected lane issues): 5 shifts x 4 K-steps, TS mode
     const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int buf = (int)(jj & 1);
-      PROF_WAIT(0, mbar_wait(&conv_full[buf], (uint32_t)((jj >> 1) & 1)));
-      if (NCOPYW) PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
+      PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
       if (jj >= 2) PROF_WAIT(1, mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * D_COLS);
@@ -388,132 +355,97 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
       uint32_t is_leader;
       asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(is_leader));
       if (is_leader) {
-        // the block-shifted A copies: TMEM lane tau, columns [split][shift q][16] <- converted block
-        // row tau + q (rows 16 B apart, so the descriptor of row q is the base + 16 q); two
-        // 128x256b copies (chunks 0-1, 2-3 of the split) per (split, shift).  A[buf] was last read
-        // by tile jj - 2's MMAs, which precede these copies in this thread's tcgen05 pipeline.
-        const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
 #pragma unroll
-        for (int split = 0; split < 2; ++split)
+        for (int qi = 0; qi < NQ; ++qi)
 #pragma unroll
-          for (int qi = 0; qi < NCP; ++qi)
-#pragma unroll
-            for (int half = 0; half < 2; ++half)
-              tmem_cp_128x256b(a0 + (uint32_t)(split * NQ * A_COLS + qi * A_COLS + half * 8),
-                               smem_desc(cv + (uint32_t)((split * 4 + half * 2) * CLBO + qi * 16), CLBO, 128));
-        // per (shift, K-step): D[0:64] += A_hi x [H_hi | H_lo] (N = 64), D[0:32] += A_lo x H_hi (N = 32)
-#pragma unroll
-        for (int qi = 0; qi < NQ; ++qi) {
-#pragma unroll
-          for (int s = 0; s < BLK / K_MMA; ++s) {
-            const uint64_t b = b0 + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4);
-            const uint32_t a = a0 + (uint32_t)(qi * A_COLS + s * (K_MMA / 2));
-            mma_ts(d, a, b, IDESC64, (qi | s) ? 1u : 0u);
-            mma_ts(d, a + (uint32_t)(NQ * A_COLS), b, IDESC32, 1u);
-          }
-        }
+          for (int s = 0; s < KI / K_MMA; ++s)
+            mma_ts(d, a0 + (uint32_t)(qi * A_COLS + s * (K_MMA / 2)),
+                   b0 + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4), IDESC64, (qi | s) ? 1u : 0u);
         mma_commit(&mma_done[buf]);
-        mma_commit(&conv_empty[buf]);                   // the cps are done with the smem tile
       }
       __syncwarp();
     }
   } else if (warp >= COPY_WARP0 && warp < COPY_WARP0 + NCOPYW) {
-    // ================= copy warps: shifts NCP..4 of TMEM lane tau (hi and lo), LDS.128 + tcgen05.st
+    // ================= copy warps: TMEM lane tau, shift q <- staged block row tau + q (32 pairs,
+    // 8 conflict-free LDS.128 through the swizzle, one tcgen05.st.x32)
     const int quarter = (warp - COPY_WARP0) & 3, part = (warp - COPY_WARP0) >> 2;
     const int tau = 32 * quarter + lane;
     const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
     constexpr int QSTEP = NCOPYW / 4;
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int buf = (int)(jj & 1);
-      PROF_WAIT(0, mbar_wait(&conv_full[buf], (uint32_t)((jj >> 1) & 1)));
+      const int slot = (int)(jj % NSTAGE), buf = (int)(jj & 1);
+      PROF_WAIT(0, mbar_wait(PS ? &stage_full[slot] : &conv_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
       if (jj >= 2) PROF_WAIT(1, mbar_wait(&mma_done[buf], (uint32_t)(((jj - 2) >> 1) & 1)));    // A[buf] free
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
+      const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
       const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS);
 #pragma unroll
-      for (int qi = NCP + part; qi < NQ; qi += QSTEP) {
-        const uint32_t row = cv + (uint32_t)((tau + qi) * 16);          // block row tau + q
-        uint4 hv[4], lv[4];
+      for (int qi = part; qi < NQ; qi += QSTEP) {
+        uint4 v[8];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          hv[g] = lds128u(row + (uint32_t)(g * CLBO));
-          lv[g] = lds128u(row + (uint32_t)((4 + g) * CLBO));
-        }
-        tmem_st16(a_col + (uint32_t)(qi * A_COLS), hv);
-        tmem_st16(a_col + (uint32_t)(NQ * A_COLS + qi * A_COLS), lv);
+        for (int g = 0; g < 8; ++g) v[g] = lds128u(st + swz(tau + qi, g));
+        tmem_st32(a_col + (uint32_t)(qi * A_COLS), v);
       }
-      mbar_arrive(&conv_empty[buf]);
+      mbar_arrive(&stage_empty[slot]);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&a_full[buf]);
     }
-  } else if (warp >= CONV_WARP0 && warp < CONV_WARP0 + CONV_WARPS) {
-    // ================= converters: staged fp32 tile -> |.| -> bf16 hi / lo, once per sample;
-    // block row r = block -2 + r; hi chunk j at j * CLBO + 16 r, lo chunk j at (4 + j) * CLBO + 16 r
+  } else if (!PS && warp >= CONV_WARP0 && warp < CONV_WARP0 + CONV_WARPS) {
+    // ================= converters (fp32 input): staged tile -> |.| -> BF16 pairs, in place
     const int ct = tid - CONV_WARP0 * 32;
+    constexpr int ITEMS = IN_BLOCKS * 8;                                     // 16-byte chunks per stage
+    constexpr int NIT = (ITEMS + CONV_THREADS - 1) / CONV_THREADS;
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int slot = (int)(jj % NSTAGE), buf = (int)(jj & 1);
+      const int slot = (int)(jj % NSTAGE);
       PROF_WAIT(0, mbar_wait(&stage_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
-      if (jj >= 2) PROF_WAIT(1, mbar_wait(&conv_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
       const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
-      const uint32_t cv = smem_u32(smem + OFF_CONV + buf * CONV_BYTES);
-      // items i = (row, fp32 chunk f) = ct + 256 k: every load of the thread first, then the
-      // splits and stores (the loads' latency overlaps instead of adding up item by item)
-      constexpr int NIT = (IN_BLOCKS * 8 + CONV_THREADS - 1) / CONV_THREADS;   // 5 (the last partial)
-      float4 v[NIT];
+      float4 v[NIT];                  // every load of the thread first, then the splits and stores
 #pragma unroll
       for (int k = 0; k < NIT; ++k) {
         const int i = ct + k * CONV_THREADS;
-        if (i < IN_BLOCKS * 8) v[k] = lds128(st + swz(i >> 3, i & 7));
+        if (i < ITEMS) v[k] = lds128(st + swz(i >> 3, i & 7));
       }
-      mbar_arrive(&stage_empty[slot]);                 // the stage is in registers: TMA may refill it
 #pragma unroll
       for (int k = 0; k < NIT; ++k) {
         const int i = ct + k * CONV_THREADS;
-        if (i >= IN_BLOCKS * 8) break;
-        const int r = i >> 3, f = i & 7;
-        uint32_t h01, l01, h23, l23;
-        split2(fabsf(v[k].x), fabsf(v[k].y), h01, l01);
-        split2(fabsf(v[k].z), fabsf(v[k].w), h23, l23);
-        const uint32_t off = (uint32_t)((f >> 1) * CLBO + r * 16 + (f & 1) * 8);
-        sts64(cv + off, h01, h23);
-        sts64(cv + off + 4 * CLBO, l01, l23);
+        if (i < ITEMS)
+          sts128u(st + swz(i >> 3, i & 7),
+                  make_uint4(split_pair(v[k].x), split_pair(v[k].y), split_pair(v[k].z), split_pair(v[k].w)));
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05.cp
-      mbar_arrive(&conv_full[buf]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before the TMA refills the slot
+      mbar_arrive(&conv_full[slot]);
     }
   } else if (warp < EPI_WARP0 + EPIW) {
     // ================= epilogue: TMEM accumulator -> clamp -> swizzled smem -> TMA store; thread =
-    // (block row tau, EPI_COLS of its 32 outputs)
-    const int quarter = (warp - EPI_WARP0) & 3, part = (warp - EPI_WARP0) >> 2;
+    // (block row tau, its 32 outputs); group g takes the tiles jj with jj % EPIG == g
+    const int quarter = (warp - EPI_WARP0) & 3, g = (warp - EPI_WARP0) >> 2;
     const int tau = 32 * quarter + lane;
-    const int et = tid - EPI_WARP0 * 32;
+    const int et = tid - EPI_WARP0 * 32 - 128 * g;
     const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
-    const uint32_t col0 = (uint32_t)(part * EPI_COLS);
-    for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int buf = (int)(jj & 1), ob = (int)(jj % NOUT);
+    for (int64_t jj = g; jj < my_tiles; jj += EPIG) {
+      const int buf = (int)(jj & 1), ob = g * NOUT_G + (int)((jj / EPIG) % NOUT_G);
       PROF_WAIT(0, mbar_wait(&mma_done[buf], (uint32_t)((jj >> 1) & 1)));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[EPI_COLS];
+      float v[BLK];
       {
-        float w[EPI_COLS];                             // (hi + lo) * h_hi  +  hi * h_lo
-        tmem_ld_cols<EPI_COLS>(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS) + col0, v);
-        tmem_ld_cols<EPI_COLS>(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS + BLK) + col0, w);
+        float w[BLK];                                  // (hi + lo) * h_hi  +  hi * h_lo
+        tmem_ld32(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS), v);
+        tmem_ld32(tmem_base + lane_off + (uint32_t)(D_COL0 + buf * D_COLS + BLK), w);
 #pragma unroll
-        for (int i = 0; i < EPI_COLS; ++i) v[i] = __fadd_rn(v[i], w[i]);
+        for (int i = 0; i < BLK; ++i) v[i] = __fadd_rn(v[i], w[i]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&d_empty[buf]);
-      if (et == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
-      named_bar(1, 32 * EPIW);
+      if (et == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT_G - 1) : "memory");
+      named_bar(1 + g, 128);
       const uint32_t osa = smem_u32(smem + OFF_OUT + ob * OUT_BYTES);
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS / 4; ++cc)
-        sts128(osa + swz(tau, (int)(col0 / 4) + cc),
-               make_float4(fmaxf(v[4 * cc], 0.f), fmaxf(v[4 * cc + 1], 0.f), fmaxf(v[4 * cc + 2], 0.f),
-                           fmaxf(v[4 * cc + 3], 0.f)));
+      for (int cc = 0; cc < BLK / 4; ++cc)
+        sts128(osa + swz(tau, cc), make_float4(fmaxf(v[4 * cc], 0.f), fmaxf(v[4 * cc + 1], 0.f),
+                                               fmaxf(v[4 * cc + 2], 0.f), fmaxf(v[4 * cc + 3], 0.f)));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 32 * EPIW);
+      named_bar(1 + g, 128);
       if (et == 0) {
         const int64_t row = tile_row(jj);
         if (out_rpf > 0)
@@ -531,8 +463,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
   }
 #ifdef DMAS_TC_PROFILE
   if (lane == 0 && blockIdx.x < 148) {
-    const int role = warp == TMA_WARP ? 0 : warp == MMA_WARP ? 1 : warp == CONV_WARP0 ? 2 : warp == EPI_WARP0 ? 3
-                   : (NCOPYW && warp == COPY_WARP0) ? 4 : -1;
+    const int role = warp == TMA_WARP ? 0 : warp == MMA_WARP ? 1 : (!PS && warp == CONV_WARP0) ? 2
+                   : warp == EPI_WARP0 ? 3 : warp == COPY_WARP0 ? 4 : -1;
     if (role >= 0) {
       g_tc_prof[blockIdx.x][role][0] = prof[0];
       g_tc_prof[blockIdx.x][role][1] = prof[1];
@@ -547,7 +479,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_envelope_tc(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
 }
 
-// ---- host: 3D tensor map [rows][nb][32] fp32 with 128-byte swizzle (driver entry point via cudart)
+// ---- host: 3D tensor map [rows][nb][32] of 4-byte samples with 128-byte swizzle (driver entry point via cudart)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -602,23 +534,43 @@ extern "C" int dmas_tc_prof_read(unsigned long long* out) {   // debug builds on
 #endif
 
 cudaError_t envelope_tc_configure() {
-  return cudaFuncSetAttribute(tc::k_envelope_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(tc::k_envelope_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tc::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tc::k_envelope_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
 }
 
-cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
-                               int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
+static cudaError_t launch_tc(bool ps, const void* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
+                             int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame,
+                             int64_t out_frame_rows) {
   const int64_t nb = T / tc::BLK;
   CUtensorMap in_map, out_map;
-  if (!tc::make_map(&in_map, y, rows, nb, tc::IN_BLOCKS)) return cudaErrorInvalidValue;
+  if (!tc::make_map(&in_map, static_cast<const float*>(y), rows, nb, tc::IN_BLOCKS)) return cudaErrorInvalidValue;
   const bool strided = out_rows_per_frame > 0;
   if (strided ? !tc::make_map_4d(&out_map, out, rows / out_rows_per_frame, out_rows_per_frame, out_frame_rows, nb)
               : !tc::make_map(&out_map, out, rows, nb, tc::TILE_BLOCKS))
     return cudaErrorInvalidValue;
   const int64_t tiles = rows * ((nb + tc::TILE_BLOCKS - 1) / tc::TILE_BLOCKS);
   const int64_t grid = tiles < sm_count ? tiles : sm_count;
-  tc::k_envelope_tc<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(in_map, out_map, rows, (int32_t)nb, taps, L,
-                                                                        strided ? out_rows_per_frame : 0);
+  const int64_t rpf = strided ? out_rows_per_frame : 0;
+  if (ps)
+    tc::k_envelope_tc<true><<<(unsigned)grid, tc::threads<true>(), tc::SMEM_BYTES, st>>>(in_map, out_map, rows,
+                                                                                       (int32_t)nb, taps, L, rpf);
+  else
+    tc::k_envelope_tc<false><<<(unsigned)grid, tc::threads<false>(), tc::SMEM_BYTES, st>>>(in_map, out_map, rows,
+                                                                                         (int32_t)nb, taps, L, rpf);
   return cudaGetLastError();
+}
+
+cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
+                               int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
+  return launch_tc(false, y, out, rows, T, taps, L, sm_count, st, out_rows_per_frame, out_frame_rows);
+}
+
+cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
+                                     int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame,
+                                     int64_t out_frame_rows) {
+  return launch_tc(true, ysplit, out, rows, T, taps, L, sm_count, st, out_rows_per_frame, out_frame_rows);
 }
 
 }  // namespace dmas

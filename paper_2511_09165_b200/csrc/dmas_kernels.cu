@@ -564,6 +564,18 @@ __device__ __forceinline__ void bf_accumulate_padded(Acc<P> (&acc)[BF_KT], uint3
   }
 }
 
+// One pixel of the split plane (BeamformArgs::split_mask): |v| as the BF16 pair (hi, lo) in one
+// 32-bit word at the pixel's fp32 position -- hi rounded half up on the magnitude, lo the BF16 of
+// the exact remainder -- with the integer round-and-mask of the envelope's converter
+// (dmas_envelope_tc.cu split_pair), so the envelope sees bit-identical operands either way.  The
+// warp's store stays one coalesced 128-byte line per block, like the fp32 image's.
+__device__ __forceinline__ uint32_t split_pair(float v) {
+  const uint32_t b = __float_as_uint(v) & 0x7FFFFFFFu;          // |v| (LOP3, not an FADD on the FMA pipe)
+  const uint32_t h = (b + 0x8000u) & 0xFFFF0000u;
+  const uint32_t l = __float_as_uint(__uint_as_float(b) - __uint_as_float(h)) + 0x8000u;
+  return __byte_perm(h, l, 0x7632);                    // hi in the low half (the lower address)
+}
+
 // Newton-Girard + CF epilogue and coalesced stores of one direction's 8 pixels.
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
 // minimal epilogue; anything else takes the generic epilogue (null-checked per kind).
@@ -571,13 +583,28 @@ template <int P, int KM, int KT = BF_KT>
 __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> (&acc)[KT], int64_t f, int64_t psi,
                                             int64_t t0, int lane) {
   const bool full_t = t0 + 32 * KT <= a.T;
-  const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
+  const int64_t row = f * a.n_dirs + psi;
+  const int64_t o = row * a.T + t0 + lane;
+  auto put = [&](int kind, int k, float v) {
+    if ((a.split_mask >> kind) & 1u) reinterpret_cast<uint32_t*>(a.out[kind])[o + 32 * k] = split_pair(v);
+    else a.out[kind][o + 32 * k] = v;
+  };
   if (KM == 4 && full_t) {
     // streaming CF-DMAS request, whole tile in range: no per-pixel guards; for p = 2 the 1/2 of
     // E_2 moves into the reciprocal, rcp(2(N B + eps)) = rcp(N B + eps)/2 exactly (power-of-two
     // scaling), so the value is bit-identical to the generic epilogue's.
-    float* dst = a.out[2] + o;
     const float n2 = (P == 2 ? 2.f : 1.f) * a.n_mics_f, e2 = (P == 2 ? 2.f : 1.f) * a.cf_eps;
+    if (a.split_mask) {                                // envelope-only request: the split plane
+      uint32_t* dst = reinterpret_cast<uint32_t*>(a.out[2]) + o;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) {
+        float A, B, E;
+        acc_final_cfdmas<P>(acc[k], A, B, E);
+        dst[32 * k] = split_pair(FM(E, FM(FM(A, A), rcp_approx(fmaf(n2, B, e2)))));
+      }
+      return;
+    }
+    float* dst = a.out[2] + o;
 #pragma unroll
     for (int k = 0; k < KT; ++k) {
       float A, B, E;
@@ -592,7 +619,7 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
       if (!full_t && t0 + lane + 32 * k >= a.T) continue;
       float A, B, E;
       acc_final<P>(acc[k], A, B, E);
-      a.out[2][o + 32 * k] = FM(E, FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps))));
+      put(2, k, FM(E, FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps)))));
     }
     return;
   }
@@ -605,8 +632,8 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
       if (!full_t && t0 + lane + 32 * k >= a.T) continue;
       float A, B, E;
       acc_final<P>(acc[k], A, B, E);
-      if (a.out[0]) a.out[0][o + 32 * k] = A;
-      if (a.out[1]) a.out[1][o + 32 * k] = E;
+      if (a.out[0]) put(0, k, A);
+      if (a.out[1]) put(1, k, E);
     }
     return;
   }
@@ -616,11 +643,11 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
     float A, B, E;
     acc_final<P>(acc[k], A, B, E);
     const float cf = FM(FM(A, A), rcp_approx(fmaf(a.n_mics_f, B, a.cf_eps)));
-    if (a.out[0]) a.out[0][o + 32 * k] = A;
-    if (a.out[1]) a.out[1][o + 32 * k] = E;
-    if (a.out[2]) a.out[2][o + 32 * k] = FM(E, cf);
-    if (a.out[3]) a.out[3][o + 32 * k] = FM(A, cf);
-    if (a.out[4]) a.out[4][o + 32 * k] = cf;
+    if (a.out[0]) put(0, k, A);
+    if (a.out[1]) put(1, k, E);
+    if (a.out[2]) put(2, k, FM(E, cf));
+    if (a.out[3]) put(3, k, FM(A, cf));
+    if (a.out[4]) put(4, k, cf);
   }
 }
 
@@ -954,8 +981,12 @@ __global__ void __launch_bounds__(BF_THREADS, (P == 2 ? DMAS_BF_MINB2 : P <= 5 ?
       const int64_t psi = a.psi_map ? (int64_t)__ldg(a.psi_map + psi0 + q) : psi0 + q;
       const int64_t o = (f * a.n_dirs + psi) * a.T + t0 + lane;
 #pragma unroll
-      for (int k = 0; k < KT; ++k)
-        if (t0 + lane + 32 * k < a.T) a.out[0][o + 32 * k] = (k & 1) ? acc[k >> 1].y : acc[k >> 1].x;
+      for (int k = 0; k < KT; ++k) {
+        if (t0 + lane + 32 * k >= a.T) continue;
+        const float v = (k & 1) ? acc[k >> 1].y : acc[k >> 1].x;
+        if (a.split_mask) reinterpret_cast<uint32_t*>(a.out[0])[o + 32 * k] = split_pair(v);
+        else a.out[0][o + 32 * k] = v;
+      }
     }
     return;
   }

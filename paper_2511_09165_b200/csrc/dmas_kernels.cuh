@@ -72,6 +72,10 @@ struct BeamformArgs {
   const int32_t* psi_map;   // LDS.64 path: tile slot psi0 + q -> image row (k-d tiles), or null (identity)
   int32_t kt;               // LDS.64 path: pixels per lane (8 or 4; 4 only without interpolation)
   int32_t l_psi;            // LDS.64 path: directions per tile (64 or 32)
+  // kinds (bit k) whose out[k] is not an fp32 image but the tensor-core envelope's input: |y| as
+  // the BF16 pair (hi, lo) in one 32-bit word per pixel (hi in the low half), same layout and size
+  // as the fp32 image.  The split is the envelope converter's (dmas_envelope_tc.cu split_pair).
+  uint32_t split_mask;
 };
 
 struct LpTaps127 { float h[128]; };
@@ -115,6 +119,10 @@ cudaError_t envelope_tc_configure();
 cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
                                int sm_count, cudaStream_t st, int64_t out_rows_per_frame = 0,
                                int64_t out_frame_rows = 0);
+// The same on a pre-split input (BeamformArgs::split_mask layout): no converter stage.
+cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
+                                     int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame = 0,
+                                     int64_t out_frame_rows = 0);
 cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out,
                                     int32_t decim, const float* lp, int32_t L, const float* bp, int32_t Lb,
                                     cudaStream_t st);

@@ -96,7 +96,8 @@ struct dmas_plan_s {
   dmas::LpTaps127 lp127{};
   bool lp_fast = false;               // FP32 FIR fast path (127 taps, R = 1, no band-pass)
   bool lp_tc = false;                 // tensor-core low-pass (L <= 127, R = 1, no band-pass)
-  int32_t env_engine = 0;             // 0 auto (tensor cores, BF16 split), 1 FP32 FIR
+  int32_t env_engine = 0;             // 0 auto (tensor cores, BF16 split), 1 FP32 FIR, 2 tensor cores on fp32 input
+  bool presplit = false;              // envelope-only kinds: the beamform writes the BF16 split plane
   int sm_count = 148;
 
   // device state
@@ -270,7 +271,7 @@ dmas_status validate(const dmas_plan_desc* d) {
   if (d->bp_taps > 0 && d->lp_taps == 0) return fail(DMAS_ERR_INVALID, "band-pass needs the envelope stage");
   if (d->env_decim < 1 || d->env_decim > 64) return fail(DMAS_ERR_INVALID, "env_decim not in [1,64]");
   if (d->scratch_bytes < 0) return fail(DMAS_ERR_INVALID, "scratch_bytes < 0");
-  if (d->env_engine < 0 || d->env_engine > 1) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1}");
+  if (d->env_engine < 0 || d->env_engine > 2) return fail(DMAS_ERR_INVALID, "env_engine not in {0, 1, 2}");
   if (d->bf_engine < 0 || d->bf_engine > 1) return fail(DMAS_ERR_INVALID, "bf_engine not in {0, 1}");
   if (d->fused_gather < 0 || d->fused_gather > 1) return fail(DMAS_ERR_INVALID, "fused_gather not in {0, 1}");
   if (d->delay_interp < 0 || d->delay_interp > 1) return fail(DMAS_ERR_INVALID, "delay_interp not in {0, 1}");
@@ -305,8 +306,13 @@ dmas_status validate(const dmas_plan_desc* d) {
 
 // Enqueue one chunk of frames: roots -> beamform -> envelopes.  `sig` / `outs_raw` / `outs_env`
 // already point at the chunk's first frame.
+//
+// `split_kinds` (a subset of the envelope-only kinds, tensor-core envelope only): raw_dst[k] is the
+// plan's scratch and the beamform writes it as the envelope's BF16 hi / lo split plane
+// (dmas_kernels.cuh BeamformArgs::split_mask), which the envelope reads without a converter stage.
 dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* const* raw_dst,
-                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st, int64_t env_frame_rows = 0) {
+                          float* const* env_dst, uint32_t env_kinds, cudaStream_t st, int64_t env_frame_rows = 0,
+                          uint32_t split_kinds = 0) {
   // DAS-only requests on the LDS.64 path sum the samples themselves: identity plane (order 1), no
   // roots (the kernel selects its DAS-only variant on the same condition, dmas_kernels.cu)
   Nvtx range("dmas chunk");
@@ -344,6 +350,7 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
   a.psi_map = p->d_psi_map;
   a.kt = p->lds_kt;
   a.l_psi = p->lds_psi;
+  a.split_mask = split_kinds;
   CUDA_TRY(timed(p, K_BEAMFORM, st, [&] { return dmas::launch_beamform(p->order, a, nf, st); }));
   if (!env_kinds) return DMAS_OK;
   cudaStream_t es = st;
@@ -355,7 +362,14 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
     const bool aligned16 = ((uintptr_t)y % 16 == 0) && ((uintptr_t)o % 16 == 0);
     if (env_frame_rows > 0 && !(p->lp_tc && aligned16))
       return fail(DMAS_ERR_CUDA, "internal: fused gather without the tensor-core envelope");
-    if (p->lp_tc && aligned16) {
+    if ((split_kinds >> k) & 1u) {
+      if (!(p->lp_tc && aligned16)) return fail(DMAS_ERR_CUDA, "internal: split plane without the tensor-core envelope");
+      CUDA_TRY(timed(p, K_ENVELOPE, es, [&] {
+        return dmas::launch_envelope_tc_split(reinterpret_cast<const uint32_t*>(y), o, rows, p->T, p->lp127,
+                                              p->lp_taps, p->sm_count, es, env_frame_rows > 0 ? p->n_dirs : 0,
+                                              env_frame_rows);
+      }));
+    } else if (p->lp_tc && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, es, [&] {
         return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->sm_count, es,
                                         env_frame_rows > 0 ? p->n_dirs : 0, env_frame_rows);
@@ -460,6 +474,14 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     }
   }
   const int32_t n_chunks = (n_frames + chunk - 1) / chunk;
+  // envelope-only kinds on the tensor-core envelope take the pre-split scratch (no converter pass)
+  // when their envelope destination meets the 16-byte alignment TMA needs
+  uint32_t split_k = 0;
+  if (p->presplit)
+    for (int i = 0; i < n; ++i)
+      if (o[i].env && ((env_only >> o[i].k) & 1u) &&
+          (fused ? (uintptr_t)mapped[i] % 16 == 0 : gather || (uintptr_t)o[i].user % 16 == 0))
+        split_k |= 1u << o[i].k;
   // under CUDA-graph capture the calls are ordered by the captured stream itself, and an event
   // recorded outside the capture must not be waited on inside it
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -502,7 +524,7 @@ dmas_status beamform_device(dmas_plan_s* p, const float* signals, int32_t n_fram
     for (int k = 0; k < dmas::N_KINDS; ++k)
       if ((env_only >> k) & 1u) raw_dst[k] = p->d_scratch + (size_t)(s++) * chunk * p->n_dirs * p->T;
     const float* sig = signals + (size_t)f0 * p->n_mics * p->T_in;
-    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, fused ? p->n_dirs_total : 0);
+    dmas_status rc = enqueue_chunk(p, sig, nf, raw_dst, env_dst, env_k, st, fused ? p->n_dirs_total : 0, split_k);
     if (rc != DMAS_OK) return rc;
     if (gather) {
       Nvtx r("dmas gather");
@@ -973,8 +995,9 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     }
     p->lp_fast = (p->lp_taps == dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 && p->T % 4 == 0);
     p->env_engine = desc->env_engine;
-    p->lp_tc = (desc->env_engine == 0 && p->lp_taps <= dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 &&
+    p->lp_tc = (desc->env_engine != 1 && p->lp_taps <= dmas::ENV_FAST_TAPS && p->bp_taps == 0 && p->env_decim == 1 &&
                 dmas::envelope_tc_supported(p->T));
+    p->presplit = p->lp_tc && desc->env_engine == 0;
     if (p->lp_fast || p->lp_tc)
       for (int i = 0; i < p->lp_taps; ++i) p->lp127.h[i] = p->h_lp[i];
     if (p->lp_tc) PLAN_TRY(dmas::envelope_tc_configure());

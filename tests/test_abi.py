@@ -96,7 +96,7 @@ def test_validation_errors(dm):
     assert _plan_err(dm, mf_coeffs=np.ones(20000)) == 2                                     # too many taps
     assert _plan_err(dm, mf_coeffs=np.array([1.0, np.inf])) == 2
     assert _plan_err(dm, bf_engine=2) == 2
-    assert _plan_err(dm, env_engine=2) == 2
+    assert _plan_err(dm, env_engine=3) == 2
     assert _plan_err(dm, delay_interp=2) == 2
 
 

@@ -520,6 +520,41 @@ def test_envelope_tc_adversarial_split_inputs(dm):
         worst = max(worst, err)
         assert_parity(env[f][None], ref[None], f"adversarial envelope row {f}")
     print(f"adversarial envelope worst error {worst:.2e} of peak")
+    # the same rows as an envelope-only request: the beamform writes the split plane itself
+    env_only = plan.beamform(torch.from_numpy(sig).cuda(), dm.ENV(dm.KIND_DAS))[("env", "das")].cpu().numpy()
+    assert np.array_equal(env_only, env)
+
+
+@pytest.mark.parametrize("p,T,interp", [(2, 4096, 0), (2, 4256, 0), (3, 96, 0), (5, 1056, 0), (2, 2080, 1)])
+def test_envelope_presplit_plane(dm, p, T, interp):
+    """Envelope-only kinds: the beamform epilogue writes |y| as the BF16 hi / lo split plane and the
+    tensor-core envelope reads it with bulk copies (no converter).  Same operands as the converter
+    path, so bitwise equal to (a) the raw + envelope request and (b) env_engine = 2 (tensor cores
+    on the fp32 image), and within the bar of the oracle.  T covers one tile per row (4096), a
+    ragged last tile (4256 = 133 blocks), a row shorter than one tile (96 = 3 blocks: both halo
+    edges in one tile) and the interpolating kernel; p = 5 the generic epilogue."""
+    import torch
+    mic = gen.disk_array(16, 0.08, 5e-3, seed=90 + p)
+    dirs = gen.az_el_grid(12, 80.0, 6, 50.0)
+    sig = gen.random_signals(2, 16, T, seed=91 + p, sparsity=0.2)
+    kinds = dm.KIND_CFDMAS | dm.KIND_DAS | (dm.KIND_CF if p == 5 else 0)
+    kw = dict(max_frames=2, delay_interp=interp)
+    x = torch.from_numpy(sig).cuda()
+    plan = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, T, **kw)
+    split = {k: v.cpu().numpy() for k, v in plan.beamform(x, dm.ENV(kinds)).items()}
+    both = {k: v.cpu().numpy() for k, v in plan.beamform(x, dm.ENV(kinds) | dm.RAW(kinds)).items()}
+    fp32in = dm.Plan(mic, dirs, gen.FS, gen.C_SOUND, p, T, env_engine=2, **kw)
+    conv = {k: v.cpu().numpy() for k, v in fp32in.beamform(x, dm.ENV(kinds)).items()}
+    torch.cuda.synchronize()
+    for key, v in split.items():
+        assert np.array_equal(v, both[key]), key
+        assert np.array_equal(v, conv[key]), key
+    if interp:
+        return                           # the interpolating path vs the oracle: test_linear_presteer_parity
+    names = [n for n, b in (("das", dm.KIND_DAS), ("cfdmas", dm.KIND_CFDMAS), ("cf", dm.KIND_CF)) if kinds & b]
+    ref = oracle_images(mic, dirs, gen.FS, gen.C_SOUND, p, sig, kinds=(), env_kinds=names)
+    for n in names:
+        assert_parity(split[("env", n)], ref[("env", n)], f"presplit p={p} T={T} {n}")
 
 
 # ------------------------------------------------------------------ NEXT-1: matched filter on the GPU

@@ -26,12 +26,13 @@ def main():
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--raw", action="store_true", help="raw CF-DMAS output instead of the envelope")
     ap.add_argument("--order", type=int, default=0, help="override the workload's DMAS order")
+    ap.add_argument("--env-engine", type=int, default=0, help="env_engine: 0 auto, 1 FP32 FIR, 2 tcgen05 on fp32")
     args = ap.parse_args()
     cfg = gen.config(args.workload, frames=min(args.frames, 4))
     sig = torch.from_numpy(cfg["signals"]).cuda()
     sig = sig.repeat((args.frames + sig.shape[0] - 1) // sig.shape[0], 1, 1)[:args.frames].contiguous()
     plan = dmas.Plan(cfg["mic_xyz"], cfg["dirs"], cfg["fs"], cfg["c"], args.order or cfg["order"], cfg["T"],
-                     max_frames=args.frames, bf_engine=args.engine)
+                     max_frames=args.frames, bf_engine=args.engine, env_engine=args.env_engine)
     what = dmas.RAW(dmas.KIND_CFDMAS) if args.raw else dmas.ENV(dmas.KIND_CFDMAS)
     outs = None
     for c in range(args.calls):
