@@ -575,6 +575,12 @@ __device__ __forceinline__ uint32_t split_pair(float v) {
   const uint32_t l = __float_as_uint(__uint_as_float(b) - __uint_as_float(h)) + 0x8000u;
   return __byte_perm(h, l, 0x7632);                    // hi in the low half (the lower address)
 }
+// the same for v >= +0 (sign bit clear): no masking
+__device__ __forceinline__ uint32_t split_pair_nonneg(float v) {
+  const uint32_t h = (__float_as_uint(v) + 0x8000u) & 0xFFFF0000u;
+  const uint32_t l = __float_as_uint(v - __uint_as_float(h)) + 0x8000u;
+  return __byte_perm(h, l, 0x7632);
+}
 
 // Newton-Girard + CF epilogue and coalesced stores of one direction's 8 pixels.
 // KM = kinds mask compiled in: DMAS_KIND_CFDMAS (4) alone is the streaming/bench case and gets a
@@ -600,7 +606,8 @@ __device__ __forceinline__ void bf_epilogue(const BeamformArgs& a, const Acc<P> 
       for (int k = 0; k < KT; ++k) {
         float A, B, E;
         acc_final_cfdmas<P>(acc[k], A, B, E);
-        dst[32 * k] = split_pair(FM(E, FM(FM(A, A), rcp_approx(fmaf(n2, B, e2)))));
+        // |E * X| = |E| * X exactly (X >= 0): the |.| is the FMUL's operand modifier
+        dst[32 * k] = split_pair_nonneg(FM(fabsf(E), FM(FM(A, A), rcp_approx(fmaf(n2, B, e2)))));
       }
       return;
     }
