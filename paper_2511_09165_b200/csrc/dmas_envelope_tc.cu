@@ -183,6 +183,12 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(src))
                : "memory");
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_NONE, version 1 (sm_100).
@@ -261,11 +267,27 @@ __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) 
 // byte offset of 16-byte chunk `c` of row `r` in a 128-byte-swizzled [rows][128 B] tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+// The constant Toeplitz blocks [B1 | B2]^T, built once per plan (envelope_tc_prepare): row n,
+// interleaved K index kk = 2k + part: B1 (n < 32) = h_hi at both parts; B2 = h_lo at part 0, 0 at
+// part 1; tap index j = n' + c - 32 q - k with n' = n mod 32.  Canonical K-major, no swizzle.
+__global__ void k_envelope_tc_taps(const __grid_constant__ LpTaps127 taps, int32_t L, uint8_t* b_image) {
+  const int c = (L - 1) / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NQ * BROWS * KI; e += gridDim.x * blockDim.x) {
+    const int qi = e / (BROWS * KI), r = e - qi * BROWS * KI, n = r / KI, kk = r - n * KI;
+    const int j = (n & (BLK - 1)) + c - BLK * (qi - HALO) - (kk >> 1);
+    uint32_t hi = 0, lo = 0;
+    if (j >= 0 && j < L) split_bf16(taps.h[j], hi, lo);
+    const uint32_t v = n < BLK ? hi : ((kk & 1) ? 0u : lo);
+    const uint32_t off = (uint32_t)(qi * B_BYTES + n * 16 + (kk >> 3) * B_LBO + (kk & 7) * 2);
+    *reinterpret_cast<uint16_t*>(b_image + off) = (uint16_t)v;
+  }
+}
+
 template <bool PS>
 __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_constant__ CUtensorMap in_map,
                                                                 const __grid_constant__ CUtensorMap out_map,
                                                                 int64_t rows, int32_t nb,
-                                                                const __grid_constant__ LpTaps127 taps, int32_t L,
+                                                                const uint8_t* __restrict__ b_image,
                                                                 int64_t out_rpf) {
   // PS: the input holds split pairs already (BeamformArgs::split_mask); else fp32 samples.
   // out_rpf > 0: the output map is 4D [frames][out_rpf rows][nb][32] with its own frame stride (a
@@ -274,7 +296,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t stage_full[NSTAGE], stage_empty[NSTAGE], conv_full[NSTAGE];
-  __shared__ __align__(8) uint64_t a_full[2], mma_done[2], d_empty[2];
+  __shared__ __align__(8) uint64_t a_full[2], mma_done[2], d_empty[2], b_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -300,24 +322,16 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
       mbar_init(&mma_done[b], 1);
       mbar_init(&d_empty[b], 32 * 4);                // the epilogue group that drains buffer b
     }
+    mbar_init(&b_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the tap blocks: one bulk copy from the plan's image (L2-resident after the first CTA)
+    mbar_expect_tx(&b_full, NQ * B_BYTES);
+    bulk_g2s(smem + OFF_B, b_image, NQ * B_BYTES, &b_full);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                  "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  // row n, interleaved K index kk = 2k + part: B1 (n < 32) = h_hi at both parts; B2 = h_lo at
-  // part 0, 0 at part 1; tap index j = n' + c - 32 q - k with n' = n mod 32
-  const int c = (L - 1) / 2;
-  for (int e = tid; e < NQ * BROWS * KI; e += THREADS) {
-    const int qi = e / (BROWS * KI), r = e - qi * BROWS * KI, n = r / KI, kk = r - n * KI;
-    const int j = (n & (BLK - 1)) + c - BLK * (qi - HALO) - (kk >> 1);
-    uint32_t hi = 0, lo = 0;
-    if (j >= 0 && j < L) split_bf16(taps.h[j], hi, lo);
-    const uint32_t v = n < BLK ? hi : ((kk & 1) ? 0u : lo);
-    const uint32_t off = (uint32_t)(qi * B_BYTES + n * 16 + (kk >> 3) * B_LBO + (kk & 7) * 2);
-    *reinterpret_cast<uint16_t*>(smem + OFF_B + off) = (uint16_t)v;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -345,6 +359,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
     // ================= MMA issuer (whole warp runs the loop so every operand is warp-uniform and
     // lives in uniform registers; one elected lane issues): 5 shifts x 4 K-steps, TS mode
     const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
+    mbar_wait(&b_full, 0);                             // the tap blocks have landed
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int buf = (int)(jj & 1);
       PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
@@ -533,6 +548,14 @@ extern "C" int dmas_tc_prof_read(unsigned long long* out) {   // debug builds on
 }
 #endif
 
+size_t envelope_tc_b_bytes() { return (size_t)tc::NQ * tc::B_BYTES; }
+
+cudaError_t envelope_tc_prepare(const LpTaps127& taps, int32_t L, void* b_image) {
+  tc::k_envelope_tc_taps<<<(tc::NQ * tc::BROWS * tc::KI + 255) / 256, 256>>>(taps, L, static_cast<uint8_t*>(b_image));
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : cudaStreamSynchronize(0);     // plan time: before any call uses it
+}
+
 cudaError_t envelope_tc_configure() {
   cudaError_t e = cudaFuncSetAttribute(tc::k_envelope_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        tc::SMEM_BYTES);
@@ -540,9 +563,9 @@ cudaError_t envelope_tc_configure() {
   return cudaFuncSetAttribute(tc::k_envelope_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
 }
 
-static cudaError_t launch_tc(bool ps, const void* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
-                             int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame,
-                             int64_t out_frame_rows) {
+static cudaError_t launch_tc(bool ps, const void* y, float* out, int64_t rows, int64_t T, const void* b_image,
+                             int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
+  if ((uintptr_t)b_image & 15u) return cudaErrorInvalidValue;
   const int64_t nb = T / tc::BLK;
   CUtensorMap in_map, out_map;
   if (!tc::make_map(&in_map, static_cast<const float*>(y), rows, nb, tc::IN_BLOCKS)) return cudaErrorInvalidValue;
@@ -553,24 +576,24 @@ static cudaError_t launch_tc(bool ps, const void* y, float* out, int64_t rows, i
   const int64_t tiles = rows * ((nb + tc::TILE_BLOCKS - 1) / tc::TILE_BLOCKS);
   const int64_t grid = tiles < sm_count ? tiles : sm_count;
   const int64_t rpf = strided ? out_rows_per_frame : 0;
+  const uint8_t* bi = static_cast<const uint8_t*>(b_image);
   if (ps)
     tc::k_envelope_tc<true><<<(unsigned)grid, tc::threads<true>(), tc::SMEM_BYTES, st>>>(in_map, out_map, rows,
-                                                                                       (int32_t)nb, taps, L, rpf);
+                                                                                       (int32_t)nb, bi, rpf);
   else
     tc::k_envelope_tc<false><<<(unsigned)grid, tc::threads<false>(), tc::SMEM_BYTES, st>>>(in_map, out_map, rows,
-                                                                                         (int32_t)nb, taps, L, rpf);
+                                                                                         (int32_t)nb, bi, rpf);
   return cudaGetLastError();
 }
 
-cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
-                               int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
-  return launch_tc(false, y, out, rows, T, taps, L, sm_count, st, out_rows_per_frame, out_frame_rows);
+cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const void* b_image, int sm_count,
+                               cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
+  return launch_tc(false, y, out, rows, T, b_image, sm_count, st, out_rows_per_frame, out_frame_rows);
 }
 
-cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
-                                     int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame,
-                                     int64_t out_frame_rows) {
-  return launch_tc(true, ysplit, out, rows, T, taps, L, sm_count, st, out_rows_per_frame, out_frame_rows);
+cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const void* b_image,
+                                     int sm_count, cudaStream_t st, int64_t out_rows_per_frame, int64_t out_frame_rows) {
+  return launch_tc(true, ysplit, out, rows, T, b_image, sm_count, st, out_rows_per_frame, out_frame_rows);
 }
 
 }  // namespace dmas

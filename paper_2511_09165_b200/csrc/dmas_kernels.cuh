@@ -114,14 +114,19 @@ cudaError_t launch_envelope_lp127(const float* y, float* out, int64_t rows, int6
 // 16-byte aligned buffers.  Persistent: one CTA per SM.
 bool envelope_tc_supported(int64_t T);
 cudaError_t envelope_tc_configure();
+// The constant Toeplitz tap blocks of the tensor-core envelope, built once per plan on the device
+// (b_image: envelope_tc_b_bytes() bytes, 16-byte aligned); every launch bulk-copies them into
+// shared memory instead of rebuilding them per CTA.
+size_t envelope_tc_b_bytes();
+cudaError_t envelope_tc_prepare(const LpTaps127& taps, int32_t L, void* b_image);
 // out_rows_per_frame > 0: `out` rows are written as [rows / out_rows_per_frame frames][out_rows_per_frame]
 // with frames out_frame_rows rows apart (a sharded plan's fused gather into the root's image).
-cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const LpTaps127& taps, int32_t L,
+cudaError_t launch_envelope_tc(const float* y, float* out, int64_t rows, int64_t T, const void* b_image,
                                int sm_count, cudaStream_t st, int64_t out_rows_per_frame = 0,
                                int64_t out_frame_rows = 0);
 // The same on a pre-split input (BeamformArgs::split_mask layout): no converter stage.
-cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const LpTaps127& taps,
-                                     int32_t L, int sm_count, cudaStream_t st, int64_t out_rows_per_frame = 0,
+cudaError_t launch_envelope_tc_split(const uint32_t* ysplit, float* out, int64_t rows, int64_t T, const void* b_image,
+                                     int sm_count, cudaStream_t st, int64_t out_rows_per_frame = 0,
                                      int64_t out_frame_rows = 0);
 cudaError_t launch_envelope_generic(const float* y, float* out, int64_t rows, int64_t T, int64_t T_out,
                                     int32_t decim, const float* lp, int32_t L, const float* bp, int32_t Lb,

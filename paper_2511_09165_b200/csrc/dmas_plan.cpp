@@ -116,6 +116,7 @@ struct dmas_plan_s {
   int32_t chunk_cap = 1;              // frames the signed-root plane holds
   float* d_splane = nullptr;
   float* d_lp = nullptr;
+  void* d_tcb = nullptr;              // tensor-core envelope: the tap blocks (dmas_kernels.cuh envelope_tc_prepare)
   float* d_bp = nullptr;
   float* d_scratch = nullptr;         // raw images of envelope-only kinds
   size_t scratch_cap = 0;
@@ -192,6 +193,7 @@ void free_plan_memory(dmas_plan_s* p) {
   cudaFree(p->d_alpha_tab);
   cudaFree(p->d_splane);
   cudaFree(p->d_lp);
+  cudaFree(p->d_tcb);
   cudaFree(p->d_bp);
   cudaFree(p->d_mf);
   cudaFree(p->d_alpha);
@@ -365,13 +367,13 @@ dmas_status enqueue_chunk(dmas_plan_s* p, const float* sig, int32_t nf, float* c
     if ((split_kinds >> k) & 1u) {
       if (!(p->lp_tc && aligned16)) return fail(DMAS_ERR_CUDA, "internal: split plane without the tensor-core envelope");
       CUDA_TRY(timed(p, K_ENVELOPE, es, [&] {
-        return dmas::launch_envelope_tc_split(reinterpret_cast<const uint32_t*>(y), o, rows, p->T, p->lp127,
-                                              p->lp_taps, p->sm_count, es, env_frame_rows > 0 ? p->n_dirs : 0,
+        return dmas::launch_envelope_tc_split(reinterpret_cast<const uint32_t*>(y), o, rows, p->T, p->d_tcb,
+                                              p->sm_count, es, env_frame_rows > 0 ? p->n_dirs : 0,
                                               env_frame_rows);
       }));
     } else if (p->lp_tc && aligned16) {
       CUDA_TRY(timed(p, K_ENVELOPE, es, [&] {
-        return dmas::launch_envelope_tc(y, o, rows, p->T, p->lp127, p->lp_taps, p->sm_count, es,
+        return dmas::launch_envelope_tc(y, o, rows, p->T, p->d_tcb, p->sm_count, es,
                                         env_frame_rows > 0 ? p->n_dirs : 0, env_frame_rows);
       }));
     } else if (p->lp_fast && aligned16) {
@@ -1000,7 +1002,11 @@ dmas_status dmas_plan(const dmas_plan_desc* desc, dmas_plan_t* out) {
     p->presplit = p->lp_tc && desc->env_engine == 0;
     if (p->lp_fast || p->lp_tc)
       for (int i = 0; i < p->lp_taps; ++i) p->lp127.h[i] = p->h_lp[i];
-    if (p->lp_tc) PLAN_TRY(dmas::envelope_tc_configure());
+    if (p->lp_tc) {
+      PLAN_TRY(dmas::envelope_tc_configure());
+      PLAN_TRY(cudaMalloc(&p->d_tcb, dmas::envelope_tc_b_bytes()));
+      PLAN_TRY(dmas::envelope_tc_prepare(p->lp127, p->lp_taps, p->d_tcb));
+    }
     PLAN_TRY(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev));
     // raw-image scratch for envelope-only kinds: the budget (default 4 GiB), capped at what
     // max_frames frames of all five kinds need, and never below one frame of every kind (sharded
