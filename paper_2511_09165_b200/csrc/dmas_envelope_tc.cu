@@ -74,6 +74,15 @@ constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (T
 #endif
 constexpr int NCOPYW = DMAS_TC_COPYW;               // 4 (one per TMEM lane quarter) or 8 (two per
 static_assert(NCOPYW == 4 || NCOPYW == 8, "COPYW"); // quarter, alternate shifts)
+// NCP = 1: shift 0 (rows 0..127 of the stage: aligned to the swizzle atom) copied into TMEM by the
+// tensor core itself (tcgen05.cp through a SWIZZLE_128B descriptor, issued by the MMA thread
+// ahead of its MMAs) and the copy warps build shifts 1..4 only.  Bitwise identical, but slower
+// (1.51 vs 1.40 ms per C5 chunk): the cps queue in front of the MMAs in the tensor pipe.
+#ifndef DMAS_TC_NCP
+#define DMAS_TC_NCP 0
+#endif
+constexpr int NCP = DMAS_TC_NCP;
+static_assert(NCP == 0 || NCP == 1, "NCP");
 #ifndef DMAS_TC_CONVW
 #define DMAS_TC_CONVW 4
 #endif
@@ -203,6 +212,16 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc_v), "r"(accumulate));
 }
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B (8-row x 128-byte atoms, SBO = 1024 B)
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// smem -> TMEM copy by the tensor core: 128 rows (lanes) x 256 bits (8 columns); asynchronous,
+// ordered with this thread's tcgen05.mma
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(desc) : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&stage_full[s], 1);
-      mbar_init(&stage_empty[s], 32 * NCOPYW);       // the copy warps' reads
+      mbar_init(&stage_empty[s], 32 * NCOPYW + NCP);   // the copy warps' reads (+ the cps' commit)
       mbar_init(&conv_full[s], CONV_THREADS);
     }
     for (int b = 0; b < 2; ++b) {
@@ -361,12 +380,27 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
     const uint64_t b0 = smem_desc(smem_u32(smem + OFF_B), B_LBO, 128);
     mbar_wait(&b_full, 0);                             // the tap blocks have landed
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
-      const int buf = (int)(jj & 1);
+      const int buf = (int)(jj & 1), slot = (int)(jj % NSTAGE);
+      const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
+      if (NCP) {
+        // shift 0 <- stage rows 0..127, four 32-byte K chunks.  A[buf] was last read by tile
+        // jj - 2's MMAs, which precede these copies in this thread's tcgen05 pipeline.
+        PROF_WAIT(0, mbar_wait(PS ? &stage_full[slot] : &conv_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t lead;
+        asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(lead));
+        if (lead) {
+          const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
+#pragma unroll
+          for (int kc = 0; kc < 4; ++kc) tmem_cp_128x256b(a0 + (uint32_t)(kc * 8), smem_desc_sw128(st + 32u * kc));
+          mma_commit(&stage_empty[slot]);              // the stage may be refilled once the cps are done
+        }
+        __syncwarp();
+      }
       PROF_WAIT(0, mbar_wait(&a_full[buf], (uint32_t)((jj >> 1) & 1)));
       if (jj >= 2) PROF_WAIT(1, mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * D_COLS);
-      const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
       uint32_t is_leader;
       asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(is_leader));
       if (is_leader) {
@@ -395,7 +429,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
       const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
       const uint32_t a_col = tmem_base + lane_off + (uint32_t)(buf * A_BUF_COLS);
 #pragma unroll
-      for (int qi = part; qi < NQ; qi += QSTEP) {
+      for (int qi = NCP + part; qi < NQ; qi += QSTEP) {
         uint4 v[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g) v[g] = lds128u(st + swz(tau + qi, g));
