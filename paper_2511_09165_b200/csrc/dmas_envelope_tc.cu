@@ -72,8 +72,16 @@ constexpr int NOUT = DMAS_TC_NOUT;                  // output staging buffers (T
 #ifndef DMAS_TC_COPYW
 #define DMAS_TC_COPYW 4
 #endif
-constexpr int NCOPYW = DMAS_TC_COPYW;               // 4 (one per TMEM lane quarter) or 8 (two per
-static_assert(NCOPYW == 4 || NCOPYW == 8, "COPYW"); // quarter, alternate shifts)
+// SS = 1: the MMAs read the five block-shifted A operands straight from the staged tile (SS mode:
+// a SWIZZLE_128B descriptor whose start address is stage row q is a valid operand, the swizzle
+// being a function of the absolute shared-memory address), so there are no copy warps and TMEM
+// holds only the accumulators; SS = 0: copy warps build the shifted copies in TMEM (TS mode).
+#ifndef DMAS_TC_SS
+#define DMAS_TC_SS 0
+#endif
+constexpr bool SS = DMAS_TC_SS != 0;
+constexpr int NCOPYW = SS ? 0 : DMAS_TC_COPYW;      // 4 (one per TMEM lane quarter) or 8 (two per
+static_assert(SS || NCOPYW == 4 || NCOPYW == 8, "COPYW");   // quarter, alternate shifts)
 // NCP = 1: shift 0 (rows 0..127 of the stage: aligned to the swizzle atom) copied into TMEM by the
 // tensor core itself (tcgen05.cp through a SWIZZLE_128B descriptor, issued by the MMA thread
 // ahead of its MMAs) and the copy warps build shifts 1..4 only.  Bitwise identical, but slower
@@ -83,6 +91,7 @@ static_assert(NCOPYW == 4 || NCOPYW == 8, "COPYW"); // quarter, alternate shifts
 #endif
 constexpr int NCP = DMAS_TC_NCP;
 static_assert(NCP == 0 || NCP == 1, "NCP");
+static_assert(!SS || NCP == 0, "NCP needs the TMEM copies");
 #ifndef DMAS_TC_CONVW
 #define DMAS_TC_CONVW 4
 #endif
@@ -117,10 +126,10 @@ constexpr int K_MMA = 16;
 // TMEM columns (32-bit): A copies [buf][shift] x 32 columns (one block row of pairs per lane), then D[buf]
 constexpr int A_COLS = BLK;                         // 32 pairs
 constexpr int A_BUF_COLS = NQ * A_COLS;             // 160
-constexpr int D_COL0 = 2 * A_BUF_COLS;              // 320: D[buf] = 64 columns (hi*h_hi + lo*h_hi | hi*h_lo)
+constexpr int D_COL0 = SS ? 0 : 2 * A_BUF_COLS;     // 320 (TS): D[buf] = 64 columns (hi*h_hi + lo*h_hi | hi*h_lo)
 constexpr int D_COLS = 2 * BLK;
 static_assert(D_COL0 + 2 * D_COLS <= 512, "TMEM columns");
-constexpr int TMEM_COLS = 512;
+constexpr int TMEM_COLS = SS ? 128 : 512;
 
 constexpr int OFF_STAGE = 0;
 constexpr int OFF_OUT = OFF_STAGE + NSTAGE * STAGE_BYTES;
@@ -286,6 +295,17 @@ __device__ __forceinline__ void split_bf16(float a, uint32_t& hi, uint32_t& lo) 
 // byte offset of 16-byte chunk `c` of row `r` in a 128-byte-swizzled [rows][128 B] tile
 __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc_v, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc_v), "r"(accumulate));
+}
+// SS-mode A operand: stage rows q .. q + 127 (block shift q - HALO), K chunk s (32 bytes = 16 bf16)
+__device__ __forceinline__ uint64_t a_desc_ss(uint32_t stage, int q, int s) {
+  return smem_desc_sw128(stage + 128u * (uint32_t)q + 32u * (uint32_t)s);
+}
+
 // The constant Toeplitz blocks [B1 | B2]^T, built once per plan (envelope_tc_prepare): row n,
 // interleaved K index kk = 2k + part: B1 (n < 32) = h_hi at both parts; B2 = h_lo at part 0, 0 at
 // part 1; tap index j = n' + c - 32 q - k with n' = n mod 32.  Canonical K-major, no swizzle.
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&stage_full[s], 1);
-      mbar_init(&stage_empty[s], 32 * NCOPYW + NCP);   // the copy warps' reads (+ the cps' commit)
+      mbar_init(&stage_empty[s], SS ? 1 : 32 * NCOPYW + NCP);   // the MMAs' commit (SS) / the copy warps' reads (+ the cps' commit)
       mbar_init(&conv_full[s], CONV_THREADS);
     }
     for (int b = 0; b < 2; ++b) {
@@ -381,6 +401,27 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
     mbar_wait(&b_full, 0);                             // the tap blocks have landed
     for (int64_t jj = 0; jj < my_tiles; ++jj) {
       const int buf = (int)(jj & 1), slot = (int)(jj % NSTAGE);
+      if (SS) {
+        PROF_WAIT(0, mbar_wait(PS ? &stage_full[slot] : &conv_full[slot], (uint32_t)((jj / NSTAGE) & 1)));
+        if (jj >= 2) PROF_WAIT(1, mbar_wait(&d_empty[buf], (uint32_t)(((jj - 2) >> 1) & 1)));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem_base + (uint32_t)(D_COL0 + buf * D_COLS);
+        const uint32_t st = smem_u32(smem + OFF_STAGE + slot * STAGE_BYTES);
+        uint32_t lead;
+        asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(lead));
+        if (lead) {
+#pragma unroll
+          for (int qi = 0; qi < NQ; ++qi)
+#pragma unroll
+            for (int s = 0; s < KI / K_MMA; ++s)
+              mma_ss(d, a_desc_ss(st, qi, s), b0 + (uint64_t)((qi * B_BYTES + 2 * s * B_LBO) >> 4), IDESC64,
+                     (qi | s) ? 1u : 0u);
+          mma_commit(&stage_empty[slot]);              // the stage may be refilled once the MMAs are done
+          mma_commit(&mma_done[buf]);
+        }
+        __syncwarp();
+        continue;
+      }
       const uint32_t a0 = tmem_base + (uint32_t)(buf * A_BUF_COLS);
       if (NCP) {
         // shift 0 <- stage rows 0..127, four 32-byte K chunks.  A[buf] was last read by tile
