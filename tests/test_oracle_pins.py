@@ -215,6 +215,26 @@ def test_cf_properties():
     assert float(O.coherence_factor(0.0, 0.0, 8)) == 0.0          # all-zero slice, eps > 0
 
 
+def test_power_sums_signed_and_newton_girard_route():
+    """P_k = sum_i s_i^k keeps the signs of odd powers (Eq. PAPER.md:131): s = (-1, 2) gives
+    (P1, P2, P3) = (1, 5, 7) by hand; and the paper's Newton-Girard expansion of those sums
+     reproduces E_3 of a mixed-sign set, e.g. E_3(-1, 2, 3) = -6 (hand value)."""
+    assert [float(v) for v in O.power_sums(np.array([-1.0, 2.0]), 3)] == [1.0, 5.0, 7.0]
+    s = np.array([-1.0, 2.0, 3.0])
+    assert float(O.newton_girard_explicit(O.power_sums(s, 3), 3)) == pytest.approx(-6.0, abs=1e-12)
+    assert float(O.esp_vieta(list(s), 3)) == -6.0
+
+
+def test_cf_default_eps_is_negligible():
+    """CF's guard is "a small, positive number" (reading Q7: 1e-30): a perfectly
+    coherent slice of tiny amplitude (x_i = 1e-9, N B = 6.4e-17) still has CF = 1 to ~1e-14, and
+    through beamform_frame's default the same holds on a one-pixel frame."""
+    x = np.full(8, 1e-9)
+    assert float(O.coherence_factor(x.sum(), (x * x).sum(), 8)) == pytest.approx(1.0, abs=1e-12)
+    img = O.beamform_frame(np.full((8, 1), 1e-9, np.float32), np.zeros((1, 8), np.int32), 2)
+    assert float(img["cf"][0, 0]) == pytest.approx(1.0, abs=1e-12)
+
+
 # ----------------------------------------------------------------- beamform_frame against per-pixel brute force
 def test_beamform_frame_bruteforce_pixels():
     """Whole chain (gather -> roots -> E_p, A, B, CF) against an independent per-pixel
