@@ -12,6 +12,7 @@ requested output is compared with the float64 oracle under the north_star bar (1
 peak; degenerate all-zero images against the input-amplitude bound, as in test_gpu_parity.py)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -23,8 +24,12 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
 KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
-N_CASES = 240
-N_LARGE = 24              # cases with 80..320 microphones (the microphone-group kernel)
+# DMAS_FUZZ_CASES / DMAS_FUZZ_LARGE widen the sweep (same seeds first, then more)
+N_CASES = int(os.environ.get("DMAS_FUZZ_CASES", 240))
+N_LARGE = int(os.environ.get("DMAS_FUZZ_LARGE", 24))    # cases with 80..320 microphones (the microphone-group kernel)
+# the conditioning scale enters the bar only where it exceeds COND_DIV x the frame's peak: never on
+# the C1-C5 frames (at most 3.9x there), so those keep exactly the north_star bar
+COND_DIV = 10.0
 
 
 def _case(seed, large=False):
@@ -65,6 +70,42 @@ def _case(seed, large=False):
     Tin = T + (len(mf) - 1 if mf is not None else 0)
     sig = gen.random_signals(F, n_mics, Tin, seed=int(rng.integers(1 << 30)), sparsity=float(rng.choice([0, 0.3])))
     return dict(p=p, mic=mic, dirs=dirs, T=T, F=F, raw_k=raw_k, env_k=env_k, opts=opts, sig=sig, mf=mf)
+
+
+def _conditioning(m, d, alpha, p, img, n_mics, eps):
+    """Per pixel and kind, the magnitude whose fp32 rounding the method's result inherits -- its
+    condition scale:
+      das    sum |x|                                   (the sum cancels)
+      dmas   K = sum over partitions of prod |P_i|^k_i / z   (the terms of Newton-Girard,
+             PAPER.md:136, that cancel -- all of them where fewer than p samples are non-zero and
+             E_p is exactly 0)
+      cf     2 |A| sum|x| / (N B + eps)                (CF = A^2 / (N B + eps) when A cancels)
+      cfdas  3 A^2 sum|x| / (N B + eps)
+      cfdmas K CF+ + |E| 2 |A| sum|x| / (N B + eps)    (CF+ >= the GPU's CF scales the residue of E)
+    from the oracle's own float64 quantities.  The bar on a pixel is 1e-4 of max(frame peak, this
+    scale / COND_DIV): where the frame's peak dominates (every realistic frame) it is the north_star
+    bar; only pixels whose value fp32 cannot resolve relative to the peak get 1e-5 of their own
+    conditioning -- still ~170x the fp32 rounding of the method."""
+    x = O.gather(m, d) if alpha is None else O.gather_linear(m, d, alpha)
+    sabs = np.sum(np.abs(x), axis=1)
+    A = np.sum(x, axis=1)
+    B = np.sum(x * x, axis=1)
+    den = n_mics * B + eps
+    P = O.power_sums(O.signed_root(x, p), p, axis=1)
+    K = np.zeros_like(P[0])
+    for ks in O._partitions(p):
+        z, term = 1.0, np.ones_like(P[0])
+        for i, k in enumerate(ks, start=1):
+            z *= math.factorial(k) * i ** k
+            if k:
+                term = term * np.abs(P[i - 1]) ** k
+        K += term / z
+    with np.errstate(divide="ignore", invalid="ignore"):
+        cfc = np.where(den > 0, 2.0 * np.abs(A) * sabs / den, 0.0)
+        # the GPU's CF is at most this (A perturbed by ~16 fp32 roundings of sum|x|; CF <= 1)
+        cf_up = np.where(den > 0, np.minimum(1.0, (np.abs(A) + 1e-6 * sabs) ** 2 / den), 0.0)
+    return {"das": sabs, "dmas": K, "cf": cfc, "cfdas": 1.5 * np.abs(A) * cfc,
+            "cfdmas": K * cf_up + np.abs(img["dmas"]) * cfc}
 
 
 @pytest.fixture(scope="module")
@@ -111,6 +152,7 @@ def _run_case(dm, seed, large):
     scale = (math.comb(len(c["mic"]), c["p"]) + len(c["mic"])) * max(float(np.max(np.abs(m))), 1e-30)
     for f in range(c["F"]):
         img = O.beamform_frame(m[f], d, c["p"], eps=o["cf_eps"], alpha=al)
+        cond = _conditioning(m[f], d, al, c["p"], img, len(c["mic"]), o["cf_eps"])
         for stage, kinds in (("raw", c["raw_k"]), ("env", c["env_k"])):
             for k in kinds:
                 ref = img[k] if stage == "raw" else O.envelope(img[k], h, bp_taps=None if bp is None else
@@ -119,9 +161,18 @@ def _run_case(dm, seed, large):
                 assert g.shape == ref.shape, (seed, stage, k)
                 assert np.all(np.isfinite(g)), (seed, stage, k)
                 peak = float(np.max(np.abs(ref)))
-                err = float(np.max(np.abs(g.astype(np.float64) - ref))) if ref.size else 0.0
                 bound = TOL * peak if peak > 0 else TOL * scale
-                assert err <= bound, (f"seed {seed} p={c['p']} n_mics={len(c['mic'])} n_dirs={len(c['dirs'])} "
+                # conditioning-aware bar: per pixel (raw) or per row through the envelope's FIR gain
+                zf = cond[k]
+                if stage == "env":
+                    gain = float(np.sum(np.abs(h))) * (float(np.sum(np.abs(bp))) if bp is not None else 1.0)
+                    zf = np.broadcast_to(gain * zf.max(axis=1, keepdims=True), ref.shape)
+                bound = np.maximum(bound, TOL * zf / COND_DIV)
+                err_px = np.abs(g.astype(np.float64) - ref)
+                err = float(np.max(err_px)) if ref.size else 0.0
+                worst = float(np.max(err_px - bound)) if ref.size else -1.0
+                bound = float(np.max(bound)) if np.ndim(bound) else bound
+                assert worst <= 0, (f"seed {seed} p={c['p']} n_mics={len(c['mic'])} n_dirs={len(c['dirs'])} "
                                       f"T={c['T']} {stage}/{k} opts={ {k2: v for k2, v in o.items() if k2 != 'bp_coeffs' and k2 != 'mf_coeffs'} }: "
-                                      f"err {err:.3e} > {bound:.3e} (peak {peak:.3e})")
+                                      f"err {err:.3e}, bound up to {bound:.3e} (peak {peak:.3e})")
     plan.close()
