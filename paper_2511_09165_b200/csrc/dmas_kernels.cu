@@ -12,7 +12,7 @@
 // cores; the one dense contraction, K4's low-pass, runs on tcgen05 (dmas_envelope_tc.cu) unless
 // the plan asks for the FP32 FIR (env_engine = 1).  K3 is bound by the FP32 pipe (5 FP32 ops per mic-pixel at p = 2) with shared-memory bandwidth
 // close behind; its staging is one cp.async.bulk (TMA bulk engine) per microphone row into a
-// window reused by BF_PSI directions; packed FADD2/FFMA2 halve the issue slots of the accumulate.
+// window reused by BF_PSI directions; packed FADD2/FFMA2 take loaded pixel pairs as they land.
 
 #include <cstdint>
 #include <cuda_runtime.h>
