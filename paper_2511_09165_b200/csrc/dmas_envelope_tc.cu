@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(threads<PS>(), 1) k_envelope_tc(const __grid_c
       mbar_init(&conv_full[s], CONV_THREADS);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&a_full[b], 32 * NCOPYW);
+      mbar_init(&a_full[b], SS ? 1 : 32 * NCOPYW);           // unused in SS mode
       mbar_init(&mma_done[b], 1);
       mbar_init(&d_empty[b], 32 * 4);                // the epilogue group that drains buffer b
     }
