@@ -9,7 +9,9 @@ LDS.64 beamformer, the tensor-core or FP32 envelope, nearest-sample or interpola
 matched filter, a band-pass, decimation, a tiny scratch budget (frame chunking) and cf_eps > 0
 (eps = 0 on all-zero pixels is 0/0; test_gpu_parity.py::test_cf_eps_zero_nonzero_input covers it).  Every
 requested output is compared with the float64 oracle under the north_star bar (1e-4 of the frame's
-peak; degenerate all-zero images against the input-amplitude bound, as in test_gpu_parity.py)."""
+peak; degenerate all-zero images against the input-amplitude bound, as in test_gpu_parity.py), except
+on pixels whose value fp32 cannot resolve next to a tiny frame peak (_conditioning, DESIGN.md
+"Parity bar"))."""
 
 import math
 import os
@@ -28,7 +30,7 @@ KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
 N_CASES = int(os.environ.get("DMAS_FUZZ_CASES", 240))
 N_LARGE = int(os.environ.get("DMAS_FUZZ_LARGE", 24))    # cases with 80..320 microphones (the microphone-group kernel)
 # the conditioning scale enters the bar only where it exceeds COND_DIV x the frame's peak: never on
-# the C1-C5 frames (at most 3.9x there), so those keep exactly the north_star bar
+# the C1-C3 frames (at most 3.9x there, measured), so those keep exactly the north_star bar
 COND_DIV = 10.0
 
 
