@@ -30,7 +30,8 @@ KINDS = ("das", "dmas", "cfdmas", "cfdas", "cf")
 N_CASES = int(os.environ.get("DMAS_FUZZ_CASES", 240))
 N_LARGE = int(os.environ.get("DMAS_FUZZ_LARGE", 24))    # cases with 80..320 microphones (the microphone-group kernel)
 # the conditioning scale enters the bar only where it exceeds COND_DIV x the frame's peak: never on
-# the C1-C3 frames (at most 3.9x there, measured), so those keep exactly the north_star bar
+# the C1-C5 frames (at most 3.9x there; C4 / C5 on sampled directions), so those keep exactly the
+# north_star bar
 COND_DIV = 10.0
 
 
