@@ -155,7 +155,7 @@ def _run_case(dm, seed, large):
     scale = (math.comb(len(c["mic"]), c["p"]) + len(c["mic"])) * max(float(np.max(np.abs(m))), 1e-30)
     for f in range(c["F"]):
         img = O.beamform_frame(m[f], d, c["p"], eps=o["cf_eps"], alpha=al)
-        cond = _conditioning(m[f], d, al, c["p"], img, len(c["mic"]), o["cf_eps"])
+        cond = None                              # computed only for a frame that needs it
         for stage, kinds in (("raw", c["raw_k"]), ("env", c["env_k"])):
             for k in kinds:
                 ref = img[k] if stage == "raw" else O.envelope(img[k], h, bp_taps=None if bp is None else
@@ -165,13 +165,16 @@ def _run_case(dm, seed, large):
                 assert np.all(np.isfinite(g)), (seed, stage, k)
                 peak = float(np.max(np.abs(ref)))
                 bound = TOL * peak if peak > 0 else TOL * scale
-                # conditioning-aware bar: per pixel (raw) or per row through the envelope's FIR gain
-                zf = cond[k]
-                if stage == "env":
-                    gain = float(np.sum(np.abs(h))) * (float(np.sum(np.abs(bp))) if bp is not None else 1.0)
-                    zf = np.broadcast_to(gain * zf.max(axis=1, keepdims=True), ref.shape)
-                bound = np.maximum(bound, TOL * zf / COND_DIV)
                 err_px = np.abs(g.astype(np.float64) - ref)
+                if ref.size and float(np.max(err_px)) > bound:
+                    # conditioning-aware bar: per pixel (raw) or per row through the envelope's FIR gain
+                    if cond is None:
+                        cond = _conditioning(m[f], d, al, c["p"], img, len(c["mic"]), o["cf_eps"])
+                    zf = cond[k]
+                    if stage == "env":
+                        gain = float(np.sum(np.abs(h))) * (float(np.sum(np.abs(bp))) if bp is not None else 1.0)
+                        zf = np.broadcast_to(gain * zf.max(axis=1, keepdims=True), ref.shape)
+                    bound = np.maximum(bound, TOL * zf / COND_DIV)
                 err = float(np.max(err_px)) if ref.size else 0.0
                 worst = float(np.max(err_px - bound)) if ref.size else -1.0
                 bound = float(np.max(bound)) if np.ndim(bound) else bound
